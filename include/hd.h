@@ -1,0 +1,121 @@
+/* hd.h -- C ABI of the B200-native DG advection hot path of hyper.deal (arXiv 2002.08110).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (the paper text and the spec written
+ * from it); Cn = reading n of DESIGN.md "Readings".
+ *
+ * What the library computes (FP64, periodic Cartesian box T = T_x (x) T_v; nodal
+ * Lagrange basis on the n = k+1 Gauss-Legendre points of each 1D reference interval [0,1],
+ * reading C1; upwind numerical flux, reading C3):
+ *   hd_apply_advection  v <- A(u), the DG weak form of Eq. into:adv:ref,
+ *                       A(u)_i = (grad phi_i, a u)_cell - sum_faces <phi_i, (a.n) u_up>_face
+ *                       (sign convention P:236, reading C4; output is the weak form, C5).
+ *   hd_apply_inv_mass   u <- M^-1 u in place (P:3, "u <- M(u)" read as M^-1, C6;
+ *                       Alg. 2 step 4 P:1095-1097, with |J| restored, C7). Collocated mass is
+ *                       diagonal: M_qq = |J| prod_i w_{q_i} (C2).
+ *   hd_apply_mass       u <- M u in place (test aid).
+ *   hd_rk_step          nsteps steps of the five-stage fourth-order low-storage Runge-Kutta
+ *                       method in the Williamson 2N form (reading C13)
+ *                       with the merged operator M^-1 A as right-hand side.
+ *   hd_fill_initial     the seeded synthetic initial data of DESIGN.md "Inputs" (reading C14).
+ *
+ * Data layout (reading C19): a DoF vector holds this rank's owned cells; cell-local DoF
+ * j = sum_i m_i n^i (dim 0 = x_1 fastest ... last v dim slowest); owned cells in the order
+ * [c_v][c_x - cx_begin], c_x and c_v lexicographic with the first axis fastest. With nranks = 1
+ * this is the global order g = c_v |C_x| + c_x. Each cell occupies n^d consecutive
+ * doubles; vectors must be 256-byte aligned device memory (cudaMalloc / torch allocations are).
+ *
+ * Ownership: every DoF vector is caller-allocated device memory of hd_mesh_info's owned_dofs
+ * doubles. The mesh owns its constant tables, halo plan and buffers, NCCL communicator and
+ * internal events; hd_destroy_mesh frees them.
+ *
+ * Streams: all work is enqueued on the given CUDA stream (cudaStream_t passed as void*; NULL =
+ * legacy default stream); calls return without host synchronisation unless stated.
+ *
+ * Errors: every call returns an hd_status; no exception crosses the ABI. hd_last_error() gives a
+ * thread-local message for the last non-OK status of the calling thread. Asynchronous CUDA
+ * faults surface on a later call as HD_ERR_CUDA. A mesh is not re-entrant (one thread at a time).
+ */
+#ifndef HD_H
+#define HD_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hd_mesh hd_mesh;
+
+typedef enum {
+  HD_OK = 0,
+  HD_ERR_ARG = -1,         /* invalid argument (dims, k, cells, box, field, aliasing, null) */
+  HD_ERR_UNSUPPORTED = -2, /* valid but not built for the GPU path (see hd_create_mesh) */
+  HD_ERR_CUDA = -3,        /* CUDA runtime error (message in hd_last_error) */
+  HD_ERR_NCCL = -4,        /* NCCL error (multi-rank halo) */
+  HD_ERR_OOM = -5,         /* device or host allocation failed */
+  HD_ERR_STATE = -6        /* call not allowed in the current state */
+} hd_status;
+
+typedef struct {
+  int d_x, d_v;         /* space dims, 1..3 each; d = d_x + d_v in 2..6 */
+  int k;                /* polynomial degree; n = k+1 in 2..6; (n,d) must satisfy n^d <= 7776 */
+  long long cells[6];   /* cells per dim, x dims first; all >= 1 */
+  double lo[6], hi[6];  /* box per dim, hi > lo; periodic in every dim (C9) */
+  double a_const[6];    /* advection field a_i(z) = a_const[i] + sum_j a_lin[i][j] z_j ...   */
+  double a_lin[36];     /* ... row-major [i][j]; a_lin[i][i] must be 0 (divergence free); the
+                           sign of a_i must be constant on every cell (reading C11) */
+  int flux;             /* 0 = upwind (the only flux built on the GPU path) */
+  int rank, nranks;     /* x-slab partition; nranks must divide |C_x| */
+  const void *nccl_id;  /* 128-byte ncclUniqueId when nranks > 1, else NULL */
+} hd_mesh_desc;
+
+/* Validate desc, build the 1D tables and the partition. HD_ERR_ARG for invalid input (S:48:
+ * invalid dim or zero subdivision; DoF-count overflow S:74); HD_ERR_UNSUPPORTED for a valid mesh
+ * outside the built kernel set. *out receives an opaque mesh; desc is copied. */
+hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out);
+hd_status hd_destroy_mesh(hd_mesh *m);
+
+/* owned_dofs: length of this rank's DoF vectors; [cx_begin, cx_end): owned range of the
+ * flattened x-cell index c_x. Any output pointer may be NULL. */
+hd_status hd_mesh_info(const hd_mesh *m, long long *owned_dofs, long long *cx_begin, long long *cx_end);
+
+/* v <- A(u) (weak form). u, v: device vectors of owned_dofs doubles that must not overlap
+ * (HD_ERR_ARG otherwise). t is the evaluation time (the built fields do not depend on t). */
+hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream);
+
+/* u <- M^-1 u and u <- M u, in place; one streaming pass, no communication. */
+hd_status hd_apply_inv_mass(hd_mesh *m, double *u, void *stream);
+hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream);
+
+/* nsteps (>= 1) LSRK(5,4) steps of size dt starting at time t. buf[0..2]: three distinct device
+ * vectors; on entry buf[*sol] holds u^n, on exit buf[*sol] holds u^{n+nsteps} (the fused stage
+ * cannot overwrite its operator input, so the solution rotates through the buffers). The other
+ * two buffers are scratch and are overwritten. */
+hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream);
+
+/* End-to-end variant with HOST buffers: copies u_host (owned_dofs doubles, ideally pinned) into
+ * dbuf[0], runs nsteps steps, copies the solution back into u_out_host (may equal u_host), and
+ * synchronises the stream before returning. dbuf: three distinct device scratch vectors. */
+hd_status hd_rk_step_host(hd_mesh *m, const double *u_host, double *u_out_host, double *dbuf[3], double t,
+                          double dt, int nsteps, void *stream);
+
+/* u <- synthetic initial data: recipe 0 gauss2d, 1 uniform, 2 sines, 3 maxwellian (DESIGN.md
+ * "Inputs"), counter-based in (seed, global DoF index), identical to the Python generator
+ * paper_2002_08110_b200/inputs.py up to libm rounding. */
+hd_status hd_fill_initial(hd_mesh *m, double *u, int recipe, unsigned long long seed, void *stream);
+
+/* Host-only queries (no GPU needed), for inspection and tests of the host plan:
+ * hd_tables_1d: the 1D tables the kernels use for n nodes (2..6): Gauss-Legendre nodes xi[n] and
+ * weights w[n] on [0,1]; the merged unit-speed upwind line operator K[2][n][n], lift lam[2][n] and
+ * neighbour-trace weights tau[2][n] (index 0: a > 0, left neighbour; 1: a < 0, right neighbour).
+ * hd_lsrk_coefficients: the 2N coefficients A_s, B_s (s = 1..5) of hd_rk_step. */
+hd_status hd_tables_1d(int n, double *xi, double *w, double *K, double *lam, double *tau);
+hd_status hd_lsrk_coefficients(double *a, double *b);
+
+/* Number of kernels this library launched since the mesh was created (bench evidence). */
+long long hd_launch_count(const hd_mesh *m);
+
+const char *hd_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HD_H */

@@ -1,0 +1,8 @@
+"""B200-native DG advection hot path of hyper.deal (arXiv 2002.08110).
+
+The product is the C-ABI library ``libhd.so`` (include/hd.h; sources in ``csrc/``), built for
+sm_100a by ``paper_2002_08110_b200.build``. ``Mesh`` is its thin Python binding. This package
+never imports the test oracle (``oracle/``) and has no CPU fallback.
+"""
+from ._binding import EXPORTS, HDError, Mesh, load_library  # noqa: F401
+from . import configs, inputs  # noqa: F401

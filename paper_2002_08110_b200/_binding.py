@@ -1,0 +1,195 @@
+"""Thin ctypes binding of libhd.so (include/hd.h). Argument marshalling only: every step of the
+hot path runs in the library's CUDA kernels. There is no CPU fallback: if libhd.so is missing or
+no CUDA device is present the calls raise."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhd.so")
+
+HD_STATUS = {0: "HD_OK", -1: "HD_ERR_ARG", -2: "HD_ERR_UNSUPPORTED", -3: "HD_ERR_CUDA", -4: "HD_ERR_NCCL",
+             -5: "HD_ERR_OOM", -6: "HD_ERR_STATE"}
+RECIPES = {"gauss2d": 0, "uniform": 1, "sines": 2, "maxwellian": 3}
+
+
+class HDError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{HD_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class HdMeshDesc(ctypes.Structure):
+    _fields_ = [
+        ("d_x", ctypes.c_int), ("d_v", ctypes.c_int), ("k", ctypes.c_int),
+        ("cells", ctypes.c_longlong * 6), ("lo", ctypes.c_double * 6), ("hi", ctypes.c_double * 6),
+        ("a_const", ctypes.c_double * 6), ("a_lin", ctypes.c_double * 36),
+        ("flux", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+        ("nccl_id", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+# every symbol include/hd.h declares (checked by tests/test_abi.py)
+EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_apply_advection", "hd_apply_inv_mass",
+           "hd_apply_mass", "hd_rk_step", "hd_rk_step_host", "hd_fill_initial", "hd_tables_1d",
+           "hd_lsrk_coefficients", "hd_launch_count", "hd_last_error"]
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libhd.so not built at {path}; run `python -m paper_2002_08110_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    vp, dp, ll = ctypes.c_void_p, P(ctypes.c_double), ctypes.c_longlong
+    lib.hd_create_mesh.argtypes = [P(HdMeshDesc), P(vp)]
+    lib.hd_destroy_mesh.argtypes = [vp]
+    lib.hd_mesh_info.argtypes = [vp, P(ll), P(ll), P(ll)]
+    lib.hd_apply_advection.argtypes = [vp, vp, vp, ctypes.c_double, vp]
+    lib.hd_apply_inv_mass.argtypes = [vp, vp, vp]
+    lib.hd_apply_mass.argtypes = [vp, vp, vp]
+    lib.hd_rk_step.argtypes = [vp, P(vp), P(ctypes.c_int), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
+    lib.hd_rk_step_host.argtypes = [vp, vp, vp, P(vp), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
+    lib.hd_fill_initial.argtypes = [vp, vp, ctypes.c_int, ctypes.c_ulonglong, vp]
+    lib.hd_tables_1d.argtypes = [ctypes.c_int, dp, dp, dp, dp, dp]
+    lib.hd_lsrk_coefficients.argtypes = [dp, dp]
+    lib.hd_launch_count.argtypes = [vp]
+    lib.hd_launch_count.restype = ll
+    lib.hd_last_error.restype = ctypes.c_char_p
+    for name in EXPORTS[:-2]:
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(st):
+    if st != 0:
+        raise HDError(st, load_library().hd_last_error().decode())
+
+
+def make_desc(spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None) -> HdMeshDesc:
+    ds = HdMeshDesc()
+    d = spec["d_x"] + spec["d_v"]
+    ds.d_x, ds.d_v, ds.k = spec["d_x"], spec["d_v"], spec["k"]
+    for i in range(d):
+        ds.cells[i] = int(spec["cells"][i])
+        ds.lo[i] = float(spec["lo"][i])
+        ds.hi[i] = float(spec["hi"][i])
+        ds.a_const[i] = float(spec["a_const"][i])
+        lin = spec.get("a_lin")
+        if lin is not None:
+            for j in range(d):
+                ds.a_lin[6 * i + j] = float(lin[i][j])
+    ds.flux = {"upwind": 0, "central": 1}[spec.get("flux", "upwind")]
+    ds.rank, ds.nranks = rank, nranks
+    ds._nccl_buf = None
+    if nccl_id is not None:
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        ds._nccl_buf = buf
+        ds.nccl_id = ctypes.cast(buf, ctypes.c_void_p)
+    return ds
+
+
+def tables_1d(n: int):
+    """Host-side 1D tables of the product path (no GPU needed)."""
+    import numpy as np
+    xi, w = np.zeros(n), np.zeros(n)
+    K, lam, tau = np.zeros((2, n, n)), np.zeros((2, n)), np.zeros((2, n))
+    P = ctypes.POINTER(ctypes.c_double)
+    _check(load_library().hd_tables_1d(n, *[a.ctypes.data_as(P) for a in (xi, w, K, lam, tau)]))
+    return dict(xi=xi, w=w, K=K, lam=lam, tau=tau)
+
+
+def lsrk_coefficients():
+    import numpy as np
+    a, b = np.zeros(5), np.zeros(5)
+    P = ctypes.POINTER(ctypes.c_double)
+    _check(load_library().hd_lsrk_coefficients(a.ctypes.data_as(P), b.ctypes.data_as(P)))
+    return a, b
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+class Mesh:
+    """A mesh of the C ABI. Vectors are torch float64 CUDA tensors of ``owned_dofs`` elements."""
+
+    def __init__(self, spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None):
+        lib = load_library()
+        self.spec = spec
+        self._desc = make_desc(spec, rank, nranks, nccl_id)
+        h = ctypes.c_void_p()
+        _check(lib.hd_create_mesh(ctypes.byref(self._desc), ctypes.byref(h)))
+        self._h = h
+        od, b, e = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
+        _check(lib.hd_mesh_info(h, ctypes.byref(od), ctypes.byref(b), ctypes.byref(e)))
+        self.owned_dofs, self.cx_begin, self.cx_end = od.value, b.value, e.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().hd_destroy_mesh(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _vec(self, x, name):
+        import torch
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+                and x.numel() == self.owned_dofs):
+            raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of {self.owned_dofs} elements")
+        return ctypes.c_void_p(x.data_ptr())
+
+    def apply_advection(self, u, v, t: float = 0.0, stream=None):
+        _check(load_library().hd_apply_advection(self._h, self._vec(u, "u"), self._vec(v, "v"), float(t),
+                                                 _stream_handle(stream)))
+        return v
+
+    def apply_inv_mass(self, u, stream=None):
+        _check(load_library().hd_apply_inv_mass(self._h, self._vec(u, "u"), _stream_handle(stream)))
+        return u
+
+    def apply_mass(self, u, stream=None):
+        _check(load_library().hd_apply_mass(self._h, self._vec(u, "u"), _stream_handle(stream)))
+        return u
+
+    def rk_step(self, bufs, sol: int, t: float, dt: float, nsteps: int = 1, stream=None) -> int:
+        arr = (ctypes.c_void_p * 3)(*[self._vec(b, f"buf[{i}]").value for i, b in enumerate(bufs)])
+        s = ctypes.c_int(sol)
+        _check(load_library().hd_rk_step(self._h, arr, ctypes.byref(s), float(t), float(dt), int(nsteps),
+                                         _stream_handle(stream)))
+        return s.value
+
+    def rk_step_host(self, u_host, u_out_host, dbufs, t: float, dt: float, nsteps: int = 1, stream=None):
+        import torch
+        for x in (u_host, u_out_host):
+            if not (isinstance(x, torch.Tensor) and not x.is_cuda and x.dtype == torch.float64
+                    and x.is_contiguous() and x.numel() == self.owned_dofs):
+                raise ValueError("host buffers must be contiguous float64 CPU tensors of owned_dofs elements")
+        arr = (ctypes.c_void_p * 3)(*[self._vec(b, f"dbuf[{i}]").value for i, b in enumerate(dbufs)])
+        _check(load_library().hd_rk_step_host(self._h, ctypes.c_void_p(u_host.data_ptr()),
+                                              ctypes.c_void_p(u_out_host.data_ptr()), arr, float(t), float(dt),
+                                              int(nsteps), _stream_handle(stream)))
+        return u_out_host
+
+    def fill_initial(self, u, recipe: str, seed: int, stream=None):
+        _check(load_library().hd_fill_initial(self._h, self._vec(u, "u"), RECIPES[recipe], int(seed),
+                                              _stream_handle(stream)))
+        return u
+
+    @property
+    def launch_count(self) -> int:
+        return int(load_library().hd_launch_count(self._h))

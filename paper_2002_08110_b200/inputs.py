@@ -44,8 +44,22 @@ def _nodes(n):
     return 0.5 * (x + 1.0)
 
 
-def cell_values(spec: dict, recipe: str, seed: int, cell_ids: np.ndarray) -> np.ndarray:
-    """Nodal values for the given global cell ids: array [len(cell_ids), n^d]."""
+def cell_values(spec: dict, recipe: str, seed: int, cell_ids: np.ndarray, chunk: int = 1 << 22) -> np.ndarray:
+    """Nodal values for the given global cell ids: array [len(cell_ids), n^d] (computed in chunks of
+    about ``chunk`` values to bound temporary memory)."""
+    d = spec["d_x"] + spec["d_v"]
+    nd = (spec["k"] + 1) ** d
+    cell_ids = np.asarray(cell_ids, dtype=np.int64).reshape(-1)
+    per = max(1, chunk // nd)
+    if len(cell_ids) <= per:
+        return _cell_values(spec, recipe, seed, cell_ids)
+    out = np.empty((len(cell_ids), nd))
+    for s in range(0, len(cell_ids), per):
+        out[s:s + per] = _cell_values(spec, recipe, seed, cell_ids[s:s + per])
+    return out
+
+
+def _cell_values(spec: dict, recipe: str, seed: int, cell_ids: np.ndarray) -> np.ndarray:
     d = spec["d_x"] + spec["d_v"]
     d_x = spec["d_x"]
     n = spec["k"] + 1
