@@ -109,9 +109,9 @@ def test_small_mesh_operators(name, spec):
     assert_close(host(vd), oracle.apply_advection(spec, u, merged=True), TOL_APPLY, name + " M^-1 A")
     w = dev(u)
     m.apply_inv_mass(w)
-    assert_close(host(w), oracle.apply_inv_mass(spec, u), 1e-15, name + " M^-1")
+    assert_close(host(w), oracle.apply_inv_mass(spec, u), 1e-14, name + " M^-1")
     m.apply_mass(w)
-    assert_close(host(w), u, 1e-15, name + " M M^-1")
+    assert_close(host(w), u, 1e-14, name + " M M^-1")
 
 
 @pytest.mark.parametrize("name,spec", SMALL[::3], ids=[s[0] for s in SMALL[::3]])
@@ -160,7 +160,7 @@ def test_config_full_parity(name):
     assert_close(host(vd), oracle.apply_advection(spec, u), TOL_APPLY, name + " A")
     w = dev(u)
     m.apply_inv_mass(w)
-    assert_close(host(w), oracle.apply_inv_mass(spec, u), 1e-15, name + " M^-1")
+    assert_close(host(w), oracle.apply_inv_mass(spec, u), 1e-14, name + " M^-1")
     # 10 RK steps (north star: <= 1e-10)
     dt = configs.time_step(spec, cfg["cfl"])
     bufs = [dev(u), torch.empty_like(ud), torch.empty_like(ud)]
@@ -252,7 +252,7 @@ def test_config_6d_sampled_parity():
     one = dict(spec, cells=[1] * 6, lo=[0.0] * 6, hi=list(h), a_lin=[[0.0] * 6 for _ in range(6)],
                a_const=[0.0] * 6)
     ref_im = np.stack([oracle.apply_inv_mass(one, own[i]) for i in range(len(ids))])
-    assert_close(host(u.view(-1, nd)[idx]), ref_im, 1e-15, "6d sampled M^-1")
+    assert_close(host(u.view(-1, nd)[idx]), ref_im, 1e-14, "6d sampled M^-1")
 
 
 def test_6d_full_rk_step_conserves_mass():
