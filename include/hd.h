@@ -110,6 +110,10 @@ hd_status hd_fill_initial(hd_mesh *m, double *u, int recipe, unsigned long long 
 hd_status hd_tables_1d(int n, double *xi, double *w, double *K, double *lam, double *tau);
 hd_status hd_lsrk_coefficients(double *a, double *b);
 
+/* Upwind-trace plan of the mesh per dimension: tmode[i] = 0 (the cell
+ * reads its upwind neighbour itself), 1 (ring of ring_slots[i] items in L2), 2 (full-size buffer). */
+hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots);
+
 /* Number of kernels this library launched since the mesh was created (bench evidence). */
 long long hd_launch_count(const hd_mesh *m);
 

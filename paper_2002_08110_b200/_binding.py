@@ -7,7 +7,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhd.so")
+LIB_PATH = os.environ.get("HD_LIB_PATH") or os.path.join(HERE, "libhd.so")
 
 HD_STATUS = {0: "HD_OK", -1: "HD_ERR_ARG", -2: "HD_ERR_UNSUPPORTED", -3: "HD_ERR_CUDA", -4: "HD_ERR_NCCL",
              -5: "HD_ERR_OOM", -6: "HD_ERR_STATE"}
@@ -35,7 +35,7 @@ _lib = None
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_apply_advection", "hd_apply_inv_mass",
            "hd_apply_mass", "hd_rk_step", "hd_rk_step_host", "hd_fill_initial", "hd_tables_1d",
-           "hd_lsrk_coefficients", "hd_launch_count", "hd_last_error"]
+           "hd_lsrk_coefficients", "hd_mesh_traces", "hd_launch_count", "hd_last_error"]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -59,6 +59,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_fill_initial.argtypes = [vp, vp, ctypes.c_int, ctypes.c_ulonglong, vp]
     lib.hd_tables_1d.argtypes = [ctypes.c_int, dp, dp, dp, dp, dp]
     lib.hd_lsrk_coefficients.argtypes = [dp, dp]
+    lib.hd_mesh_traces.argtypes = [vp, P(ctypes.c_int), P(ctypes.c_int)]
     lib.hd_launch_count.argtypes = [vp]
     lib.hd_launch_count.restype = ll
     lib.hd_last_error.restype = ctypes.c_char_p
@@ -189,6 +190,12 @@ class Mesh:
         _check(load_library().hd_fill_initial(self._h, self._vec(u, "u"), RECIPES[recipe], int(seed),
                                               _stream_handle(stream)))
         return u
+
+    def traces(self):
+        d = self.spec["d_x"] + self.spec["d_v"]
+        tm, rs = (ctypes.c_int * 6)(), (ctypes.c_int * 6)()
+        _check(load_library().hd_mesh_traces(self._h, tm, rs))
+        return list(tm)[:d], list(rs)[:d]
 
     @property
     def launch_count(self) -> int:

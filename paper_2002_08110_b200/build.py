@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhd.so")
 SOURCES = ["hd_api.cpp", "hd_tables.cpp", "hd_kernels.cu"]
-HEADERS = ["hd_internal.h", os.path.join("..", "..", "include", "hd.h")]
+HEADERS = ["hd_internal.h", "hd_cell.cuh", os.path.join("..", "..", "include", "hd.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

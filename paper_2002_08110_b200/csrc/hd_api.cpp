@@ -2,9 +2,11 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <utility>
 
 #include "hd_internal.h"
 
@@ -45,28 +47,123 @@ hd_status ensure_tables(hd_mesh *m) {
   return HD_OK;
 }
 
-void fill_cell_params(const hd_mesh *m, hd::CellParams &p) {
+void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   std::memset(&p, 0, sizeof(p));
   const int d = m->d;
-  p.ncells = m->ncells_local;
-  p.cells_per_batch = hd::cells_per_batch(d, m->n);
-  p.nbatches = (p.ncells + p.cells_per_batch - 1) / p.cells_per_batch;
+  const int C = m->geo.C;
+  p.ncells = (int)m->ncells_local;
+  p.nitems = (int)(m->ncells_local / C);
   p.jdet = m->jdet;
-  p.nx_local = m->nx_local;
-  p.cx_begin = m->cx_begin;
-  p.d_x = m->desc.d_x;
-  long long stride = 1;
+  if (const char *dbg = getenv("HD_DEBUG")) p.debug = atoi(dbg);
+  int lstride = 1, istride = 1;
   for (int i = 0; i < d; ++i) {
-    p.L[i] = m->desc.cells[i];
+    p.L[i] = (int)m->desc.cells[i];
+    p.IL[i] = i == 0 ? p.L[0] / C : p.L[i];
+    p.lstride[i] = lstride;
+    p.istride[i] = istride;
+    lstride *= p.L[i];
+    istride *= p.IL[i];
     p.lo[i] = m->desc.lo[i];
     p.h[i] = m->h[i];
     p.inv_h[i] = 1.0 / m->h[i];
     p.a_const[i] = m->desc.a_const[i];
     for (int j = 0; j < d; ++j) p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
-    if (i == m->desc.d_x) stride = m->nx_local;  // v dims: strides in units of the local slab
-    p.lstride[i] = stride;
-    stride *= m->desc.cells[i];
+    p.tmode[i] = m->tmode[i];
+    p.dirneg[i] = m->tmode[i] != hd::kTraceNone ? m->dirneg[i] : 0;
+    p.rmask[i] = m->rmask[i];
+    p.tbuf[i] = m->tbuf[i];
   }
+  p.flags = m->flags;
+  // publication mask: phase ph (dims 2ph, 2ph+1) is published when one of its dims has traces
+  // (consumers acquire it) or a ring dim of phase ph-1 checks it before overwriting a slot
+  const int nph = m->geo.phases;
+  for (int i = 0; i < d; ++i) {
+    const int ph = i / 2;
+    if (m->tmode[i] != hd::kTraceNone) p.pubmask |= 1 << ph;
+    if (m->tmode[i] == hd::kTraceRing) p.pubmask |= 1 << (ph + 1);
+  }
+  (void)nph;
+  // one epoch per cell-kernel launch; flags count warp publications cumulatively
+  m->epoch += 1;
+  p.target = (int)(m->epoch * m->geo.warps_per_item);
+}
+
+// Upwind-trace plan: a dim can use published traces when its speed
+// sign depends only on slower dims (then the traversal can follow it); dims sorted by item stride
+// get an L2-resident ring while the ring budget lasts, the rest a full-size buffer.
+hd_status plan_traces(hd_mesh *m) {
+  const int d = m->d;
+  const hd::CellGeometry &g = m->geo;
+  const long long fn = m->nd / m->n;  // face points
+  int istride[6], IL0 = (int)(m->desc.cells[0] / g.C);
+  long long st = 1;
+  for (int i = 0; i < d; ++i) {
+    istride[i] = (int)st;
+    st *= i == 0 ? IL0 : m->desc.cells[i];
+  }
+  const long long nitems = m->ncells_local / g.C;
+  double budget = 64.0 * (1 << 20);
+  if (const char *e = getenv("HD_RING_MB")) budget = atof(e) * (1 << 20);
+  bool use = true;
+  if (const char *e = getenv("HD_TRACE")) use = atoi(e) != 0;
+  int order[6];
+  for (int i = 0; i < d; ++i) order[i] = i;
+  for (int i = 0; i < d; ++i)
+    for (int j = i + 1; j < d; ++j)
+      if (istride[order[j]] < istride[order[i]]) std::swap(order[i], order[j]);
+  double used = 0.0;
+  for (int oi = 0; oi < d; ++oi) {
+    const int i = order[oi];
+    m->tmode[i] = hd::kTraceNone;
+    m->rmask[i] = 0;
+    m->tbuf[i] = nullptr;
+    // eligible: the sign of a_i is the same on the whole box, so the traversal can follow it in
+    // every cell with one global direction (then the producer of a cell's upwind trace is exactly
+    // istride_i items earlier); a_i is affine, so check its extreme values at the box corners
+    double amin = m->desc.a_const[i], amax = m->desc.a_const[i];
+    for (int j = 0; j < d; ++j) {
+      const double aj = m->desc.a_lin[6 * i + j];
+      amin += fmin(aj * m->desc.lo[j], aj * m->desc.hi[j]);
+      amax += fmax(aj * m->desc.lo[j], aj * m->desc.hi[j]);
+    }
+    m->dirneg[i] = amax <= 0.0 && amin < 0.0 ? 1 : 0;
+    const bool eligible = use && m->desc.cells[i] > 1 && (amin >= 0.0 || amax <= 0.0);
+    if (!eligible) continue;
+    long long R = 1;
+    while (R < (long long)istride[i] + 2LL * m->grid + 64) R <<= 1;
+    const double ring_bytes = (double)R * g.C * fn * 8.0;
+    size_t bytes;
+    if (R < nitems && used + ring_bytes <= budget) {
+      m->tmode[i] = hd::kTraceRing;
+      m->rmask[i] = (int)(R - 1);
+      used += ring_bytes;
+      bytes = (size_t)ring_bytes;
+    } else {
+      m->tmode[i] = hd::kTraceFar;
+      bytes = (size_t)nitems * g.C * fn * 8;
+    }
+    cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+    }
+  }
+  const size_t fbytes = (size_t)nitems * (g.phases + 1) * sizeof(int);
+  cudaError_t e = cudaMalloc(&m->flags, fbytes);
+  if (e == cudaSuccess) e = cudaMemset(m->flags, 0, fbytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HD_ERR_OOM, "flag buffer: %s", cudaGetErrorString(e));
+  }
+  m->epoch = 0;
+  return HD_OK;
+}
+
+void free_mesh(hd_mesh *m) {
+  for (int i = 0; i < 6; ++i)
+    if (m->tbuf[i]) cudaFree(m->tbuf[i]);
+  if (m->flags) cudaFree(m->flags);
+  delete m;
 }
 
 bool overlaps(const void *a, const void *b, size_t bytes) {
@@ -183,13 +280,37 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     return st;
   }
   m->launches = 0;
+  if (m->ncells_local >= (1LL << 31) || m->owned_dofs / m->n >= (1LL << 40)) {
+    delete m;
+    return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
+  }
+  m->geo = hd::cell_geometry(d, n, (int)desc->cells[0]);
+  e = hd::cell_grid_size(d, n, (int)desc->cells[0], 0, m->sms, &m->grid);
+  if (e != cudaSuccess) {
+    delete m;
+    return cuda_fail(e, "cell kernel occupancy");
+  }
+  st = plan_traces(m);
+  if (st != HD_OK) {
+    free_mesh(m);
+    return st;
+  }
   *out = m;
   return HD_OK;
 }
 
 hd_status hd_destroy_mesh(hd_mesh *m) {
   if (!m) return fail(HD_ERR_ARG, "null mesh");
-  delete m;
+  free_mesh(m);
+  return HD_OK;
+}
+
+hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots) {
+  if (!m) return fail(HD_ERR_ARG, "null mesh");
+  for (int i = 0; i < m->d; ++i) {
+    if (tmode) tmode[i] = m->tmode[i];
+    if (ring_slots) ring_slots[i] = m->tmode[i] == hd::kTraceRing ? m->rmask[i] + 1 : 0;
+  }
   return HD_OK;
 }
 
@@ -242,7 +363,7 @@ hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, v
   p.out = v;
   p.mode = hd::kModeAdvection;
   p.dtfac = 1.0;
-  cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->sms);
+  cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->grid);
   if (e != cudaSuccess) return cuda_fail(e, "advection kernel");
   return HD_OK;
 }
@@ -290,7 +411,12 @@ hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, 
       p.mode = s == 0 ? hd::kModeRKFirst : hd::kModeRK;
       p.rk_a = kRkA[s];
       p.rk_b = kRkB[s];
-      cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->sms);
+      // every launch is a new publication epoch for the trace flags
+      if (step > 0 || s > 0) {
+        m->epoch += 1;
+        p.target = (int)(m->epoch * m->geo.warps_per_item);
+      }
+      cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->grid);
       if (e != cudaSuccess) return cuda_fail(e, "rk stage kernel");
       const int tmp = iu;
       iu = iw;

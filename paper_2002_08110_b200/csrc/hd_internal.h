@@ -32,26 +32,40 @@ void build_tables(int n, Tables1D &t);
 
 enum Mode : int { kModeAdvection = 0, kModeRK = 1, kModeRKFirst = 2 };
 
+// Trace mode of a dimension:
+//   kTraceNone: every consumer reads its upwind neighbour cell and forms the trace itself
+//   kTraceRing: producers publish downwind traces into an L2-resident ring of items
+//   kTraceFar : producers publish into a full-size buffer (consumer is many items later)
+enum TraceMode : int { kTraceNone = 0, kTraceRing = 1, kTraceFar = 2 };
+
 // Kernel parameters (passed by value as __grid_constant__).
 struct CellParams {
   const double *u;        // operator input (never written by the kernel)
   double *out;            // A-mode: v; RK-mode: U_new
   double *du;             // RK-mode: dU (read unless first stage, written)
-  long long ncells;       // owned cells
-  long long nbatches;     // ceil(ncells / cells_per_batch)
-  int cells_per_batch;
+  int ncells;             // owned cells (< 2^31)
+  int nitems;             // work items = ncells / C (C consecutive cells along dim 0)
   int mode;
+  int target;             // flag value that marks "published in this launch" (epoch * warps per item)
   double rk_a, rk_b;      // stage coefficients A_s, B_s
   double dtfac;           // 1 (A-mode) or dt (RK-mode): folded into the line speeds
   double jdet;            // |J| = prod h_i
-  // geometry
-  long long L[kMaxD];     // cells per dim (global)
-  long long lstride[kMaxD];  // local cell-index stride per dim
-  long long nx_local, cx_begin;
+  // geometry (local box of cells)
+  int L[kMaxD];           // cells per dim
+  int IL[kMaxD];          // item-grid extents (IL[0] = L[0] / C)
+  int istride[kMaxD];     // item-index stride per dim (traversal order)
+  int lstride[kMaxD];     // cell-index stride per dim (memory order)
   double lo[kMaxD], h[kMaxD], inv_h[kMaxD];
   double a_const[kMaxD];
   double a_lin[kMaxD][kMaxD];
-  int d_x;
+  // upwind traces
+  int tmode[kMaxD];       // TraceMode per dim
+  int dirneg[kMaxD];      // traversal direction of trace dims: 1 if a_i < 0 everywhere
+  int rmask[kMaxD];       // ring slots - 1 (kTraceRing)
+  double *tbuf[kMaxD];    // trace storage per dim: [slot][cell in item][n^(d-1)]
+  int *flags;             // [nitems][phases + 1] publication counters
+  int pubmask;            // bit ph: phase ph's counter is waited on (publish it)
+  int debug;
 };
 
 // Stream kernels
@@ -75,11 +89,17 @@ struct FillParams {
 
 // Launchers (hd_kernels.cu). Return cudaError_t of the launch; *launches incremented.
 cudaError_t upload_tables(int n, const Tables1D &t);
-cudaError_t launch_cell_kernel(int d, int n, const CellParams &p, cudaStream_t s, long long *launches, int sms);
+cudaError_t launch_cell_kernel(int d, int n, const CellParams &p, cudaStream_t s, long long *launches, int grid);
 cudaError_t launch_mass_kernel(int d, int n, const StreamParams &p, cudaStream_t s, long long *launches, int sms);
 cudaError_t launch_fill_kernel(int d, int n, const FillParams &p, cudaStream_t s, long long *launches);
 bool cell_kernel_supported(int d, int n);
-int cells_per_batch(int d, int n);
+// Kernel geometry for (d, n, L0): cells per item C (a divisor of L0), threads per CTA, phases,
+// warps per item, and the persistent grid size (co-resident CTAs).
+struct CellGeometry {
+  int C, threads, phases, warps_per_item, smem;
+};
+CellGeometry cell_geometry(int d, int n, int L0);
+cudaError_t cell_grid_size(int d, int n, int L0, int mode, int sms, int *grid);
 
 }  // namespace hd
 
@@ -95,4 +115,11 @@ struct hd_mesh {
   hd::Tables1D tab;
   int device, sms;
   long long launches;
+  // trace machinery (device buffers owned by the mesh)
+  hd::CellGeometry geo;
+  int tmode[6], rmask[6], dirneg[6];
+  double *tbuf[6];
+  int *flags;
+  long long epoch;
+  int grid;
 };
