@@ -63,8 +63,12 @@ typedef struct {
   double a_lin[36];     /* ... row-major [i][j]; a_lin[i][i] must be 0 (divergence free); the
                            sign of a_i must be constant on every cell (reading C11) */
   int flux;             /* 0 = upwind (the only flux built on the GPU path) */
-  int rank, nranks;     /* x-slab partition; nranks must divide |C_x| */
-  const void *nccl_id;  /* 128-byte ncclUniqueId when nranks > 1, else NULL */
+  int rank, nranks;     /* x-space partition over nranks ranks: the ranks form a grid
+                           xparts[0] x .. x xparts[d_x-1] over the x-cells; every v-cell is rank-local */
+  const void *nccl_id;  /* 128-byte ncclUniqueId when nranks > 1 and the NCCL transport is wanted; NULL
+                           selects the in-process loopback transport (hd_*_group calls) */
+  int xparts[3];        /* ranks per x dim (p_i must divide cells[i], prod = nranks); all 0 = automatic:
+                           the factorisation with the smallest halo, x-slabs (slowest dim) on ties */
 } hd_mesh_desc;
 
 /* Validate desc, build the 1D tables and the partition. HD_ERR_ARG for invalid input (S:48:
@@ -76,6 +80,11 @@ hd_status hd_destroy_mesh(hd_mesh *m);
 /* owned_dofs: length of this rank's DoF vectors; [cx_begin, cx_end): owned range of the
  * flattened x-cell index c_x. Any output pointer may be NULL. */
 hd_status hd_mesh_info(const hd_mesh *m, long long *owned_dofs, long long *cx_begin, long long *cx_end);
+
+/* The rank's local box of the global cell grid: off[i], len[i] per dim (d entries used; v dims are never
+ * split) and the rank grid xparts[3]. Local vectors hold the box's cells lexicographically (first axis
+ * fastest). Any output pointer may be NULL. */
+hd_status hd_mesh_box(const hd_mesh *m, long long *off, long long *len, int *xparts);
 
 /* v <- A(u) (weak form). u, v: device vectors of owned_dofs doubles that must not overlap
  * (HD_ERR_ARG otherwise). t is the evaluation time (the built fields do not depend on t). */
@@ -90,6 +99,14 @@ hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream);
  * cannot overwrite its operator input, so the solution rotates through the buffers). The other
  * two buffers are scratch and are overwritten. */
 hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream);
+
+/* Multi-rank meshes WITHOUT an NCCL communicator (desc.nccl_id == NULL): all P ranks' meshes live in
+ * this process on the current device and the halo is moved by device copies (loopback transport, the
+ * same buffer layout NCCL delivers). ms[r] must be rank r of P. u, v: P device vectors;
+ * bufs: 3P device vectors (rank r uses bufs[3r .. 3r+2]); *sol as in hd_rk_step (common to all ranks). */
+hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double **v, double t, void *stream);
+hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double t, double dt, int nsteps,
+                           void *stream);
 
 /* End-to-end variant with HOST buffers: copies u_host (owned_dofs doubles, ideally pinned) into
  * dbuf[0], runs nsteps steps, copies the solution back into u_out_host (may equal u_host), and
@@ -113,6 +130,18 @@ hd_status hd_lsrk_coefficients(double *a, double *b);
 /* Upwind-trace plan of the mesh per dimension: tmode[i] = 0 (the cell
  * reads its upwind neighbour itself), 1 (ring of ring_slots[i] items in L2), 2 (full-size buffer). */
 hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots);
+
+/* 128-byte ncclUniqueId for hd_mesh_desc.nccl_id (rank 0 creates it and broadcasts it). Loads
+ * libnccl.so.2 at run time; HD_ERR_NCCL if it is unavailable. */
+hd_status hd_nccl_unique_id(void *out128);
+
+/* Host-only plan queries (no GPU): the partition of desc->rank (xparts[3], off[6], len[6]) and its halo
+ * lists along x dim `dim`: which = 0 traces sent to the left rank, 1 sent to the right rank (ids = global
+ * ids of the RECEIVING cells, in message order), 2 received from the left rank, 3 from the right rank
+ * (ids = global ids of this rank's receiving cells, in buffer order). *count: capacity of ids in, length
+ * out (ids may be NULL to query the length); *peer: the partner rank (-1 if the dim is not split). */
+hd_status hd_partition_info(const hd_mesh_desc *desc, int *xparts, long long *off, long long *len);
+hd_status hd_halo_list(const hd_mesh_desc *desc, int dim, int which, long long *ids, long long *count, int *peer);
 
 /* Number of kernels this library launched since the mesh was created (bench evidence). */
 long long hd_launch_count(const hd_mesh *m);

@@ -26,16 +26,17 @@ class HdMeshDesc(ctypes.Structure):
         ("cells", ctypes.c_longlong * 6), ("lo", ctypes.c_double * 6), ("hi", ctypes.c_double * 6),
         ("a_const", ctypes.c_double * 6), ("a_lin", ctypes.c_double * 36),
         ("flux", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
-        ("nccl_id", ctypes.c_void_p),
+        ("nccl_id", ctypes.c_void_p), ("xparts", ctypes.c_int * 3),
     ]
 
 
 _lib = None
 
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_apply_advection", "hd_apply_inv_mass",
-           "hd_apply_mass", "hd_rk_step", "hd_rk_step_host", "hd_fill_initial", "hd_tables_1d",
-           "hd_lsrk_coefficients", "hd_mesh_traces", "hd_launch_count", "hd_last_error"]
+EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection",
+           "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_step_host", "hd_apply_advection_group",
+           "hd_rk_step_group", "hd_fill_initial", "hd_tables_1d", "hd_lsrk_coefficients", "hd_mesh_traces",
+           "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_launch_count", "hd_last_error"]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -60,6 +61,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_tables_1d.argtypes = [ctypes.c_int, dp, dp, dp, dp, dp]
     lib.hd_lsrk_coefficients.argtypes = [dp, dp]
     lib.hd_mesh_traces.argtypes = [vp, P(ctypes.c_int), P(ctypes.c_int)]
+    lib.hd_mesh_box.argtypes = [vp, P(ll), P(ll), P(ctypes.c_int)]
+    lib.hd_apply_advection_group.argtypes = [P(vp), ctypes.c_int, P(vp), P(vp), ctypes.c_double, vp]
+    lib.hd_rk_step_group.argtypes = [P(vp), ctypes.c_int, P(vp), P(ctypes.c_int), ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_int, vp]
+    lib.hd_nccl_unique_id.argtypes = [vp]
+    lib.hd_partition_info.argtypes = [P(HdMeshDesc), P(ctypes.c_int), P(ll), P(ll)]
+    lib.hd_halo_list.argtypes = [P(HdMeshDesc), ctypes.c_int, ctypes.c_int, P(ll), P(ll), P(ctypes.c_int)]
     lib.hd_launch_count.argtypes = [vp]
     lib.hd_launch_count.restype = ll
     lib.hd_last_error.restype = ctypes.c_char_p
@@ -74,7 +82,8 @@ def _check(st):
         raise HDError(st, load_library().hd_last_error().decode())
 
 
-def make_desc(spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None) -> HdMeshDesc:
+def make_desc(spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
+              xparts=None) -> HdMeshDesc:
     ds = HdMeshDesc()
     d = spec["d_x"] + spec["d_v"]
     ds.d_x, ds.d_v, ds.k = spec["d_x"], spec["d_v"], spec["k"]
@@ -89,12 +98,42 @@ def make_desc(spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None 
                 ds.a_lin[6 * i + j] = float(lin[i][j])
     ds.flux = {"upwind": 0, "central": 1}[spec.get("flux", "upwind")]
     ds.rank, ds.nranks = rank, nranks
+    if xparts is not None:
+        for i, p in enumerate(xparts):
+            ds.xparts[i] = int(p)
     ds._nccl_buf = None
     if nccl_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         ds._nccl_buf = buf
         ds.nccl_id = ctypes.cast(buf, ctypes.c_void_p)
     return ds
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it and broadcasts it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().hd_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def partition_info(spec: dict, rank: int, nranks: int, xparts=None):
+    """Host-only: (xparts[3], box offset[d], box length[d]) of a rank (no GPU needed)."""
+    d = spec["d_x"] + spec["d_v"]
+    ds = make_desc(spec, rank, nranks, None, xparts)
+    xp, off, ln = (ctypes.c_int * 3)(), (ctypes.c_longlong * 6)(), (ctypes.c_longlong * 6)()
+    _check(load_library().hd_partition_info(ctypes.byref(ds), xp, off, ln))
+    return list(xp), list(off)[:d], list(ln)[:d]
+
+
+def halo_list(spec: dict, rank: int, nranks: int, dim: int, which: int, xparts=None):
+    """Host-only halo plan query (include/hd.h hd_halo_list): (peer, [global cell ids])."""
+    ds = make_desc(spec, rank, nranks, None, xparts)
+    lib = load_library()
+    cnt, peer = ctypes.c_longlong(0), ctypes.c_int(0)
+    _check(lib.hd_halo_list(ctypes.byref(ds), dim, which, None, ctypes.byref(cnt), ctypes.byref(peer)))
+    ids = (ctypes.c_longlong * max(1, cnt.value))()
+    _check(lib.hd_halo_list(ctypes.byref(ds), dim, which, ids, ctypes.byref(cnt), ctypes.byref(peer)))
+    return peer.value, list(ids)[:cnt.value]
 
 
 def tables_1d(n: int):
@@ -125,16 +164,21 @@ def _stream_handle(stream):
 class Mesh:
     """A mesh of the C ABI. Vectors are torch float64 CUDA tensors of ``owned_dofs`` elements."""
 
-    def __init__(self, spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None, xparts=None):
         lib = load_library()
         self.spec = spec
-        self._desc = make_desc(spec, rank, nranks, nccl_id)
+        self.rank, self.nranks = rank, nranks
+        self._desc = make_desc(spec, rank, nranks, nccl_id, xparts)
         h = ctypes.c_void_p()
         _check(lib.hd_create_mesh(ctypes.byref(self._desc), ctypes.byref(h)))
         self._h = h
         od, b, e = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
         _check(lib.hd_mesh_info(h, ctypes.byref(od), ctypes.byref(b), ctypes.byref(e)))
         self.owned_dofs, self.cx_begin, self.cx_end = od.value, b.value, e.value
+        d = spec["d_x"] + spec["d_v"]
+        off, ln, xp = (ctypes.c_longlong * 6)(), (ctypes.c_longlong * 6)(), (ctypes.c_int * 3)()
+        _check(lib.hd_mesh_box(h, off, ln, xp))
+        self.box_off, self.box_len, self.xparts = list(off)[:d], list(ln)[:d], list(xp)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -200,3 +244,24 @@ class Mesh:
     @property
     def launch_count(self) -> int:
         return int(load_library().hd_launch_count(self._h))
+
+
+def apply_advection_group(meshes, us, vs, t: float = 0.0, stream=None):
+    """Loopback multi-rank v <- A(u): meshes[r] is rank r of P (no NCCL), all on the current device."""
+    P = len(meshes)
+    ms = (ctypes.c_void_p * P)(*[m._h.value for m in meshes])
+    ua = (ctypes.c_void_p * P)(*[m._vec(u, "u").value for m, u in zip(meshes, us)])
+    va = (ctypes.c_void_p * P)(*[m._vec(v, "v").value for m, v in zip(meshes, vs)])
+    _check(load_library().hd_apply_advection_group(ms, P, ua, va, float(t), _stream_handle(stream)))
+
+
+def rk_step_group(meshes, bufs, sol: int, t: float, dt: float, nsteps: int = 1, stream=None) -> int:
+    """Loopback multi-rank LSRK steps; bufs[r] = the 3 buffers of rank r. Returns the new sol."""
+    P = len(meshes)
+    ms = (ctypes.c_void_p * P)(*[m._h.value for m in meshes])
+    flat = [m._vec(b, "buf").value for m, bs in zip(meshes, bufs) for b in bs]
+    arr = (ctypes.c_void_p * (3 * P))(*flat)
+    s = ctypes.c_int(sol)
+    _check(load_library().hd_rk_step_group(ms, P, arr, ctypes.byref(s), float(t), float(dt), int(nsteps),
+                                           _stream_handle(stream)))
+    return s.value

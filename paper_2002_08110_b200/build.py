@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhd.so")
-SOURCES = ["hd_api.cpp", "hd_tables.cpp", "hd_kernels.cu"]
+SOURCES = ["hd_api.cpp", "hd_plan.cpp", "hd_tables.cpp", "hd_kernels.cu"]
 HEADERS = ["hd_internal.h", "hd_cell.cuh", os.path.join("..", "..", "include", "hd.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -35,8 +35,9 @@ def needs_build() -> bool:
     return False
 
 
-def build(force: bool = False, verbose_ptxas: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose_ptxas: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile csrc/ into ``out``. ``defines``: extra -D flags (experiments; the product uses none)."""
+    if not force and out == LIB and not needs_build():
         return LIB
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
@@ -44,16 +45,19 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         obj = os.path.join(HERE, "build", src + ".o")
         cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-c",
                os.path.join(CSRC, src), "-o", obj, "-I", os.path.join(ROOT, "include")]
+        cmd += [f"-D{x}" for x in defines]
         if verbose_ptxas and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
-    os.replace(tmp, LIB)
-    return LIB
+    tmp = out + f".tmp{os.getpid()}"
+    subprocess.check_call([_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"])
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose_ptxas="--verbose-ptxas" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose_ptxas="--verbose-ptxas" in sys.argv,
+                out=os.path.join(HERE, outs[0]) if outs else LIB, defines=defs))

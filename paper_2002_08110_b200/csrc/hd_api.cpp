@@ -1,4 +1,6 @@
 // hd_api.cpp -- the C ABI (include/hd.h): validation, mesh/partition plan, LSRK(5,4) driver.
+#include <dlfcn.h>
+
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -6,7 +8,9 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <string>
 #include <utility>
+#include <vector>
 
 #include "hd_internal.h"
 
@@ -34,6 +38,61 @@ const double kRkB[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 136
                         1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
                         2277821191437.0 / 14882151754819.0};
 
+// ---- NCCL, loaded at run time (only multi-rank meshes with a ncclUniqueId need it; torch's NCCL is
+// picked up when it is already loaded). Minimal prototypes of the stable NCCL C API.
+typedef struct {
+  char internal[128];
+} nccl_unique_id;
+typedef int nccl_result;
+constexpr int kNcclFloat64 = 8;
+
+}  // namespace
+
+namespace hd {
+struct NcclApi {
+  bool ok = false;
+  nccl_result (*get_unique_id)(nccl_unique_id *) = nullptr;
+  nccl_result (*comm_init_rank)(void **, int, nccl_unique_id, int) = nullptr;
+  nccl_result (*comm_destroy)(void *) = nullptr;
+  nccl_result (*send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  nccl_result (*recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  nccl_result (*group_start)() = nullptr;
+  nccl_result (*group_end)() = nullptr;
+  const char *(*error_string)(nccl_result) = nullptr;
+};
+}  // namespace hd
+
+namespace {
+
+hd::NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+hd_status load_nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.ok) return HD_OK;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(HD_ERR_NCCL, "cannot load libnccl.so.2: %s", dlerror());
+#define HD_SYM(field, name)                                                        \
+  *(void **)(&g_nccl.field) = dlsym(h, name);                                      \
+  if (!g_nccl.field) return fail(HD_ERR_NCCL, "libnccl.so.2 lacks %s", name);
+  HD_SYM(get_unique_id, "ncclGetUniqueId")
+  HD_SYM(comm_init_rank, "ncclCommInitRank")
+  HD_SYM(comm_destroy, "ncclCommDestroy")
+  HD_SYM(send, "ncclSend")
+  HD_SYM(recv, "ncclRecv")
+  HD_SYM(group_start, "ncclGroupStart")
+  HD_SYM(group_end, "ncclGroupEnd")
+  HD_SYM(error_string, "ncclGetErrorString")
+#undef HD_SYM
+  g_nccl.ok = true;
+  return HD_OK;
+}
+
+hd_status nccl_fail(nccl_result r, const char *what) {
+  return fail(HD_ERR_NCCL, "%s: %s", what, g_nccl.error_string ? g_nccl.error_string(r) : "?");
+}
+
 std::mutex g_tab_mu;
 unsigned g_tab_uploaded[64];  // per device: bitmask of n whose tables are in constant memory
 
@@ -50,110 +109,95 @@ hd_status ensure_tables(hd_mesh *m) {
 void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   std::memset(&p, 0, sizeof(p));
   const int d = m->d;
-  const int C = m->geo.C;
-  p.ncells = (int)m->ncells_local;
-  p.nitems = (int)(m->ncells_local / C);
+  const hd::CellGeometry &g = m->geo;
+  p.CT = g.CT;
+  p.GPU = g.GPU;
+  p.pencil = g.pencil;
+  p.UC = g.pencil ? (int)m->pt.len[0] : g.CT;
+  p.nunits = m->nunits;
   p.jdet = m->jdet;
-  if (const char *dbg = getenv("HD_DEBUG")) p.debug = atoi(dbg);
-  int lstride = 1, istride = 1;
+  int lstride = 1, ustride = 1;
   for (int i = 0; i < d; ++i) {
-    p.L[i] = (int)m->desc.cells[i];
-    p.IL[i] = i == 0 ? p.L[0] / C : p.L[i];
+    p.L[i] = (int)m->pt.len[i];
+    p.coff[i] = (int)m->pt.off[i];
+    p.xsplit[i] = i < 3 && m->pt.xparts[i] > 1 ? 1 : 0;
+    if (p.xsplit[i]) {
+      p.hbuf[i] = m->hbuf[i];
+      p.hslot[i] = m->hslot[i];
+    }
     p.lstride[i] = lstride;
-    p.istride[i] = istride;
     lstride *= p.L[i];
-    istride *= p.IL[i];
+    if (i >= 1) {
+      p.ustride[i] = ustride;
+      ustride *= p.L[i];
+    }
     p.lo[i] = m->desc.lo[i];
     p.h[i] = m->h[i];
     p.inv_h[i] = 1.0 / m->h[i];
     p.a_const[i] = m->desc.a_const[i];
     for (int j = 0; j < d; ++j) p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
-    p.tmode[i] = m->tmode[i];
-    p.dirneg[i] = m->tmode[i] != hd::kTraceNone ? m->dirneg[i] : 0;
-    p.rmask[i] = m->rmask[i];
+    p.pub[i] = m->pub[i];
+    p.dirneg[i] = m->pub[i] ? m->dirneg[i] : 0;
     p.tbuf[i] = m->tbuf[i];
+    p.pubany |= m->pub[i];
   }
   p.flags = m->flags;
-  // publication mask: phase ph (dims 2ph, 2ph+1) is published when one of its dims has traces
-  // (consumers acquire it) or a ring dim of phase ph-1 checks it before overwriting a slot
-  const int nph = m->geo.phases;
-  for (int i = 0; i < d; ++i) {
-    const int ph = i / 2;
-    if (m->tmode[i] != hd::kTraceNone) p.pubmask |= 1 << ph;
-    if (m->tmode[i] == hd::kTraceRing) p.pubmask |= 1 << (ph + 1);
-  }
-  (void)nph;
-  // one epoch per cell-kernel launch; flags count warp publications cumulatively
+  // one epoch per cell-kernel launch: unit flags hold the epoch of their last completion
   m->epoch += 1;
-  p.target = (int)(m->epoch * m->geo.warps_per_item);
+  p.epoch = (int)m->epoch;
 }
 
-// Upwind-trace plan: a dim can use published traces when its speed
-// sign depends only on slower dims (then the traversal can follow it); dims sorted by item stride
-// get an L2-resident ring while the ring budget lasts, the rest a full-size buffer.
+// Upwind-trace plan (DESIGN.md §6 "Upwind traces"). In pencil mode a dim i >= 1 publishes its traces
+// when (a) the sign of a_i is the same on the whole box (the traversal then follows it, so the producer
+// of a cell's upwind trace is exactly ustride_i units earlier) and (b) that producer is at least
+// HD_PUB_MIN (default 2) x grid units earlier, i.e. certainly finished in the steady state. All other
+// dims read their upwind neighbour cell themselves (it is then recent enough to be in L2).
 hd_status plan_traces(hd_mesh *m) {
   const int d = m->d;
   const hd::CellGeometry &g = m->geo;
   const long long fn = m->nd / m->n;  // face points
-  int istride[6], IL0 = (int)(m->desc.cells[0] / g.C);
-  long long st = 1;
-  for (int i = 0; i < d; ++i) {
-    istride[i] = (int)st;
-    st *= i == 0 ? IL0 : m->desc.cells[i];
-  }
-  const long long nitems = m->ncells_local / g.C;
-  double budget = 64.0 * (1 << 20);
-  if (const char *e = getenv("HD_RING_MB")) budget = atof(e) * (1 << 20);
   bool use = true;
   if (const char *e = getenv("HD_TRACE")) use = atoi(e) != 0;
-  int order[6];
-  for (int i = 0; i < d; ++i) order[i] = i;
-  for (int i = 0; i < d; ++i)
-    for (int j = i + 1; j < d; ++j)
-      if (istride[order[j]] < istride[order[i]]) std::swap(order[i], order[j]);
-  double used = 0.0;
-  for (int oi = 0; oi < d; ++oi) {
-    const int i = order[oi];
-    m->tmode[i] = hd::kTraceNone;
-    m->rmask[i] = 0;
+  double pub_min = 2.0;
+  if (const char *e = getenv("HD_PUB_MIN")) pub_min = atof(e);
+  long long ustride = 1;
+  bool any = false;
+  for (int i = 0; i < d; ++i) {
+    m->pub[i] = 0;
+    m->dirneg[i] = 0;
     m->tbuf[i] = nullptr;
-    // eligible: the sign of a_i is the same on the whole box, so the traversal can follow it in
-    // every cell with one global direction (then the producer of a cell's upwind trace is exactly
-    // istride_i items earlier); a_i is affine, so check its extreme values at the box corners
-    double amin = m->desc.a_const[i], amax = m->desc.a_const[i];
-    for (int j = 0; j < d; ++j) {
-      const double aj = m->desc.a_lin[6 * i + j];
-      amin += fmin(aj * m->desc.lo[j], aj * m->desc.hi[j]);
-      amax += fmax(aj * m->desc.lo[j], aj * m->desc.hi[j]);
-    }
-    m->dirneg[i] = amax <= 0.0 && amin < 0.0 ? 1 : 0;
-    const bool eligible = use && m->desc.cells[i] > 1 && (amin >= 0.0 || amax <= 0.0);
-    if (!eligible) continue;
-    long long R = 1;
-    while (R < (long long)istride[i] + 2LL * m->grid + 64) R <<= 1;
-    const double ring_bytes = (double)R * g.C * fn * 8.0;
-    size_t bytes;
-    if (R < nitems && used + ring_bytes <= budget) {
-      m->tmode[i] = hd::kTraceRing;
-      m->rmask[i] = (int)(R - 1);
-      used += ring_bytes;
-      bytes = (size_t)ring_bytes;
-    } else {
-      m->tmode[i] = hd::kTraceFar;
-      bytes = (size_t)nitems * g.C * fn * 8;
-    }
-    cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+    if (i >= 1) {
+      const long long us = ustride;
+      ustride *= m->pt.len[i];
+      if (!use || !g.pencil || m->pt.len[i] < 2 || (i < 3 && m->pt.xparts[i] > 1)) continue;
+      double amin = m->desc.a_const[i], amax = m->desc.a_const[i];
+      for (int j = 0; j < d; ++j) {
+        const double aj = m->desc.a_lin[6 * i + j];
+        amin += fmin(aj * m->desc.lo[j], aj * m->desc.hi[j]);
+        amax += fmax(aj * m->desc.lo[j], aj * m->desc.hi[j]);
+      }
+      if (!(amin >= 0.0 || amax <= 0.0)) continue;
+      if ((double)us < pub_min * m->grid) continue;
+      m->pub[i] = 1;
+      m->dirneg[i] = amax <= 0.0 && amin < 0.0 ? 1 : 0;
+      const size_t bytes = (size_t)m->ncells_local * fn * sizeof(double);
+      cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+      }
+      any = true;
     }
   }
-  const size_t fbytes = (size_t)nitems * (g.phases + 1) * sizeof(int);
-  cudaError_t e = cudaMalloc(&m->flags, fbytes);
-  if (e == cudaSuccess) e = cudaMemset(m->flags, 0, fbytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(HD_ERR_OOM, "flag buffer: %s", cudaGetErrorString(e));
+  m->flags = nullptr;
+  if (any) {
+    const size_t fbytes = (size_t)m->nunits * sizeof(int);
+    cudaError_t e = cudaMalloc(&m->flags, fbytes);
+    if (e == cudaSuccess) e = cudaMemset(m->flags, 0, fbytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HD_ERR_OOM, "flag buffer: %s", cudaGetErrorString(e));
+    }
   }
   m->epoch = 0;
   return HD_OK;
@@ -163,7 +207,124 @@ void free_mesh(hd_mesh *m) {
   for (int i = 0; i < 6; ++i)
     if (m->tbuf[i]) cudaFree(m->tbuf[i]);
   if (m->flags) cudaFree(m->flags);
+  for (int i = 0; i < 3; ++i) {
+    if (m->hbuf[i]) cudaFree(m->hbuf[i]);
+    if (m->hslot[i]) cudaFree(m->hslot[i]);
+  }
+  if (m->pack_cells) cudaFree(m->pack_cells);
+  if (m->pack_dimsg) cudaFree(m->pack_dimsg);
+  if (m->sendbuf) cudaFree(m->sendbuf);
+  if (m->nccl_comm && g_nccl.ok) g_nccl.comm_destroy(m->nccl_comm);
   delete m;
+}
+
+template <class T>
+hd_status upload(T **dst, const T *src, size_t count, const char *what) {
+  *dst = nullptr;
+  if (count == 0) return HD_OK;
+  cudaError_t e = cudaMalloc(dst, count * sizeof(T));
+  if (e == cudaSuccess && src) e = cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HD_ERR_OOM, "%s (%zu bytes): %s", what, count * sizeof(T), cudaGetErrorString(e));
+  }
+  return HD_OK;
+}
+
+// Halo plan and buffers of a multi-rank mesh (hd_plan.cpp).
+hd_status setup_halo(hd_mesh *m) {
+  const long long fn = m->nd / m->n;
+  std::vector<int> cells, dimsg;
+  for (int i = 0; i < m->desc.d_x; ++i) {
+    hd::HaloDim &hd = m->halo[i];
+    hd::make_halo(m->desc, m->pt, m->h, i, hd);
+    if (!hd.active) continue;
+    // send buffer per dim: [to the right rank (a_i > 0, tau of the right face)][to the left rank]
+    m->send_off_right[i] = (long long)cells.size();
+    for (int c : hd.send_right) {
+      cells.push_back(c);
+      dimsg.push_back(i);
+    }
+    m->send_off_left[i] = (long long)cells.size();
+    for (int c : hd.send_left) {
+      cells.push_back(c);
+      dimsg.push_back(i | (1 << 8));
+    }
+    hd_status st = upload(&m->hslot[i], hd.slot.data(), hd.slot.size(), "halo slot table");
+    if (st != HD_OK) return st;
+    st = upload(&m->hbuf[i], (const double *)nullptr, (size_t)(hd.n_from_left + hd.n_from_right) * fn,
+                "halo receive buffer");
+    if (st != HD_OK) return st;
+  }
+  m->nsend = (long long)cells.size();
+  hd_status st = upload(&m->pack_cells, cells.data(), cells.size(), "halo pack list");
+  if (st == HD_OK) st = upload(&m->pack_dimsg, dimsg.data(), dimsg.size(), "halo pack list");
+  if (st == HD_OK) st = upload(&m->sendbuf, (const double *)nullptr, (size_t)m->nsend * fn, "halo send buffer");
+  return st;
+}
+
+// Pack the outgoing traces of u (every stage: the operator input changes).
+hd_status halo_pack(hd_mesh *m, const double *u, cudaStream_t s) {
+  if (m->nsend == 0) return HD_OK;
+  hd::PackParams pp;
+  pp.u = u;
+  pp.out = m->sendbuf;
+  pp.cells = m->pack_cells;
+  pp.dimsg = m->pack_dimsg;
+  pp.nent = m->nsend;
+  cudaError_t e = hd::launch_pack_kernel(m->d, m->n, pp, s, &m->launches);
+  if (e != cudaSuccess) return cuda_fail(e, "halo pack kernel");
+  return HD_OK;
+}
+
+// NCCL transport: one group per exchange; per peer the order is canonical on both sides (dims
+// ascending; per dim: send to the right before send to the left, receive from the left before receive
+// from the right), so every send meets its receive even when left == right (two ranks along a dim).
+hd_status halo_exchange_nccl(hd_mesh *m, cudaStream_t s) {
+  const long long fn = m->nd / m->n;
+  nccl_result r = g_nccl.group_start();
+  if (r) return nccl_fail(r, "ncclGroupStart");
+  for (int i = 0; i < m->desc.d_x; ++i) {
+    const hd::HaloDim &hd = m->halo[i];
+    if (!hd.active) continue;
+    const size_t nr = hd.send_right.size() * fn, nl = hd.send_left.size() * fn;
+    if (nr) r = g_nccl.send(m->sendbuf + m->send_off_right[i] * fn, nr, kNcclFloat64, hd.right, m->nccl_comm, s);
+    if (!r && nl) r = g_nccl.send(m->sendbuf + m->send_off_left[i] * fn, nl, kNcclFloat64, hd.left, m->nccl_comm, s);
+    if (!r && hd.n_from_left)
+      r = g_nccl.recv(m->hbuf[i], hd.n_from_left * fn, kNcclFloat64, hd.left, m->nccl_comm, s);
+    if (!r && hd.n_from_right)
+      r = g_nccl.recv(m->hbuf[i] + hd.n_from_left * fn, hd.n_from_right * fn, kNcclFloat64, hd.right, m->nccl_comm, s);
+    if (r) {
+      g_nccl.group_end();
+      return nccl_fail(r, "ncclSend/ncclRecv");
+    }
+  }
+  r = g_nccl.group_end();
+  if (r) return nccl_fail(r, "ncclGroupEnd");
+  return HD_OK;
+}
+
+// Loopback transport (all ranks' meshes in this process on one device): device copies from each
+// neighbour's send buffer into the receive buffer, in the same layout NCCL would deliver.
+hd_status halo_exchange_loopback(hd_mesh **ms, int P, cudaStream_t s) {
+  for (int r = 0; r < P; ++r) {
+    hd_mesh *m = ms[r];
+    const long long fn = m->nd / m->n;
+    for (int i = 0; i < m->desc.d_x; ++i) {
+      const hd::HaloDim &hd = m->halo[i];
+      if (!hd.active) continue;
+      const hd_mesh *L = ms[hd.left], *R = ms[hd.right];
+      cudaError_t e = cudaSuccess;
+      if (hd.n_from_left)
+        e = cudaMemcpyAsync(m->hbuf[i], L->sendbuf + L->send_off_right[i] * fn, hd.n_from_left * fn * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess && hd.n_from_right)
+        e = cudaMemcpyAsync(m->hbuf[i] + hd.n_from_left * fn, R->sendbuf + R->send_off_left[i] * fn,
+                            hd.n_from_right * fn * sizeof(double), cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "loopback halo copy");
+    }
+  }
+  return HD_OK;
 }
 
 bool overlaps(const void *a, const void *b, size_t bytes) {
@@ -208,9 +369,11 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     return fail(HD_ERR_UNSUPPORTED, "(d=%d, n=%d) is not in the built kernel set", d, n);
   if (desc->nranks < 1 || desc->rank < 0 || desc->rank >= desc->nranks)
     return fail(HD_ERR_ARG, "rank %d / nranks %d invalid", desc->rank, desc->nranks);
-  if (cx_total % desc->nranks != 0)
-    return fail(HD_ERR_ARG, "nranks (%d) must divide |C_x| (%lld)", desc->nranks, cx_total);
-  if (desc->nranks > 1) return fail(HD_ERR_UNSUPPORTED, "multi-rank halo not built yet");
+  hd::Partition pt;
+  {
+    std::string err;
+    if (!hd::make_partition(*desc, pt, err)) return fail(HD_ERR_ARG, "%s", err.c_str());
+  }
   // the sign of each a_i must be constant on every cell (reading C11): check the affine field's
   // range over each 1D cell slab of the dims it depends on
   for (int i = 0; i < d; ++i) {
@@ -250,14 +413,25 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   m->d = d;
   m->n = n;
   m->nd = nd;
+  m->pt = pt;
   m->ncells_global = ncells;
   m->cx_total = cx_total;
-  m->nx_local = cx_total / desc->nranks;
-  m->cx_begin = m->nx_local * desc->rank;
-  m->cx_end = m->cx_begin + m->nx_local;
-  m->nv = ncells / cx_total;
-  m->ncells_local = m->nx_local * m->nv;
+  m->ncells_local = pt.ncells_local;
   m->owned_dofs = m->ncells_local * nd;
+  {
+    // flat x-cell range of the local box when it is contiguous (x-slab or one rank), else -1
+    long long lo = 0, st = 1, cnt = 1;
+    for (int i = 0; i < desc->d_x; ++i) {
+      lo += pt.off[i] * st;
+      st *= desc->cells[i];
+      cnt *= pt.len[i];
+    }
+    bool contiguous = true;
+    for (int i = 0; i + 1 < desc->d_x; ++i)
+      if (pt.xparts[i] > 1) contiguous = false;
+    m->cx_begin = contiguous ? lo : -1;
+    m->cx_end = contiguous ? lo + cnt : -1;
+  }
   m->jdet = 1.0;
   for (int i = 0; i < d; ++i) {
     m->h[i] = (desc->hi[i] - desc->lo[i]) / (double)desc->cells[i];
@@ -280,17 +454,31 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     return st;
   }
   m->launches = 0;
-  if (m->ncells_local >= (1LL << 31) || m->owned_dofs / m->n >= (1LL << 40)) {
+  if (m->ncells_local >= (1LL << 31)) {
     delete m;
     return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
   }
-  m->geo = hd::cell_geometry(d, n, (int)desc->cells[0]);
-  e = hd::cell_grid_size(d, n, (int)desc->cells[0], 0, m->sms, &m->grid);
+  m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local);
+  m->nunits = (int)(m->geo.pencil ? m->ncells_local / pt.len[0] : m->ncells_local / m->geo.CT);
+  e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
   if (e != cudaSuccess) {
     delete m;
     return cuda_fail(e, "cell kernel occupancy");
   }
   st = plan_traces(m);
+  if (st == HD_OK && desc->nranks > 1) st = setup_halo(m);
+  if (st == HD_OK && desc->nranks > 1 && desc->nccl_id) {
+    st = load_nccl();
+    if (st == HD_OK) {
+      nccl_unique_id id;
+      std::memcpy(&id, desc->nccl_id, sizeof(id));
+      nccl_result r = g_nccl.comm_init_rank(&m->nccl_comm, desc->nranks, id, desc->rank);
+      if (r) {
+        m->nccl_comm = nullptr;
+        st = nccl_fail(r, "ncclCommInitRank");
+      }
+    }
+  }
   if (st != HD_OK) {
     free_mesh(m);
     return st;
@@ -308,17 +496,9 @@ hd_status hd_destroy_mesh(hd_mesh *m) {
 hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots) {
   if (!m) return fail(HD_ERR_ARG, "null mesh");
   for (int i = 0; i < m->d; ++i) {
-    if (tmode) tmode[i] = m->tmode[i];
-    if (ring_slots) ring_slots[i] = m->tmode[i] == hd::kTraceRing ? m->rmask[i] + 1 : 0;
+    if (tmode) tmode[i] = m->pub[i] ? 2 : 0;
+    if (ring_slots) ring_slots[i] = 0;
   }
-  return HD_OK;
-}
-
-hd_status hd_mesh_info(const hd_mesh *m, long long *owned_dofs, long long *cx_begin, long long *cx_end) {
-  if (!m) return fail(HD_ERR_ARG, "null mesh");
-  if (owned_dofs) *owned_dofs = m->owned_dofs;
-  if (cx_begin) *cx_begin = m->cx_begin;
-  if (cx_end) *cx_end = m->cx_end;
   return HD_OK;
 }
 
@@ -349,25 +529,6 @@ hd_status hd_lsrk_coefficients(double *a, double *b) {
   return HD_OK;
 }
 
-long long hd_launch_count(const hd_mesh *m) { return m ? m->launches : -1; }
-
-hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream) {
-  (void)t;
-  if (!m || !u || !v) return fail(HD_ERR_ARG, "null argument");
-  if (overlaps(u, v, (size_t)m->owned_dofs * sizeof(double))) return fail(HD_ERR_ARG, "u and v overlap");
-  hd_status st = ensure_tables(m);
-  if (st != HD_OK) return st;
-  hd::CellParams p;
-  fill_cell_params(m, p);
-  p.u = u;
-  p.out = v;
-  p.mode = hd::kModeAdvection;
-  p.dtfac = 1.0;
-  cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->grid);
-  if (e != cudaSuccess) return cuda_fail(e, "advection kernel");
-  return HD_OK;
-}
-
 static hd_status mass_impl(hd_mesh *m, double *u, void *stream, int inverse) {
   if (!m || !u) return fail(HD_ERR_ARG, "null argument");
   hd_status st = ensure_tables(m);
@@ -382,50 +543,10 @@ static hd_status mass_impl(hd_mesh *m, double *u, void *stream, int inverse) {
   return HD_OK;
 }
 
+long long hd_launch_count(const hd_mesh *m) { return m ? m->launches : -1; }
+
 hd_status hd_apply_inv_mass(hd_mesh *m, double *u, void *stream) { return mass_impl(m, u, stream, 1); }
 hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream) { return mass_impl(m, u, stream, 0); }
-
-hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {
-  (void)t;
-  if (!m || !buf || !sol) return fail(HD_ERR_ARG, "null argument");
-  if (*sol < 0 || *sol > 2) return fail(HD_ERR_ARG, "*sol must be 0, 1 or 2");
-  if (nsteps < 1) return fail(HD_ERR_ARG, "nsteps must be >= 1");
-  if (!std::isfinite(dt)) return fail(HD_ERR_ARG, "dt not finite");
-  const size_t bytes = (size_t)m->owned_dofs * sizeof(double);
-  for (int i = 0; i < 3; ++i) {
-    if (!buf[i]) return fail(HD_ERR_ARG, "null buffer %d", i);
-    for (int j = 0; j < i; ++j)
-      if (overlaps(buf[i], buf[j], bytes)) return fail(HD_ERR_ARG, "buffers %d and %d overlap", j, i);
-  }
-  hd_status st = ensure_tables(m);
-  if (st != HD_OK) return st;
-  hd::CellParams p;
-  fill_cell_params(m, p);
-  p.dtfac = dt;
-  int iu = *sol, idu = (*sol + 1) % 3, iw = (*sol + 2) % 3;
-  for (int step = 0; step < nsteps; ++step) {
-    for (int s = 0; s < 5; ++s) {
-      p.u = buf[iu];
-      p.du = buf[idu];
-      p.out = buf[iw];
-      p.mode = s == 0 ? hd::kModeRKFirst : hd::kModeRK;
-      p.rk_a = kRkA[s];
-      p.rk_b = kRkB[s];
-      // every launch is a new publication epoch for the trace flags
-      if (step > 0 || s > 0) {
-        m->epoch += 1;
-        p.target = (int)(m->epoch * m->geo.warps_per_item);
-      }
-      cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->grid);
-      if (e != cudaSuccess) return cuda_fail(e, "rk stage kernel");
-      const int tmp = iu;
-      iu = iw;
-      iw = tmp;
-    }
-  }
-  *sol = iu;
-  return HD_OK;
-}
 
 hd_status hd_rk_step_host(hd_mesh *m, const double *u_host, double *u_out_host, double *dbuf[3], double t, double dt,
                           int nsteps, void *stream) {
@@ -444,6 +565,259 @@ hd_status hd_rk_step_host(hd_mesh *m, const double *u_host, double *u_out_host, 
   return HD_OK;
 }
 
+hd_status hd_mesh_info(const hd_mesh *m, long long *owned_dofs, long long *cx_begin, long long *cx_end) {
+  if (!m) return fail(HD_ERR_ARG, "null mesh");
+  if (owned_dofs) *owned_dofs = m->owned_dofs;
+  if (cx_begin) *cx_begin = m->cx_begin;
+  if (cx_end) *cx_end = m->cx_end;
+  return HD_OK;
+}
+
+hd_status hd_mesh_box(const hd_mesh *m, long long *off, long long *len, int *xparts) {
+  if (!m) return fail(HD_ERR_ARG, "null mesh");
+  for (int i = 0; i < 6; ++i) {
+    if (off) off[i] = i < m->d ? m->pt.off[i] : 0;
+    if (len) len[i] = i < m->d ? m->pt.len[i] : 1;
+  }
+  for (int i = 0; i < 3; ++i)
+    if (xparts) xparts[i] = m->pt.xparts[i];
+  return HD_OK;
+}
+
+hd_status hd_nccl_unique_id(void *out) {
+  if (!out) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = load_nccl();
+  if (st != HD_OK) return st;
+  nccl_unique_id id;
+  nccl_result r = g_nccl.get_unique_id(&id);
+  if (r) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof(id));
+  return HD_OK;
+}
+
+hd_status hd_partition_info(const hd_mesh_desc *desc, int *xparts, long long *off, long long *len) {
+  if (!desc) return fail(HD_ERR_ARG, "null argument");
+  if (desc->nranks < 1 || desc->rank < 0 || desc->rank >= desc->nranks)
+    return fail(HD_ERR_ARG, "rank %d / nranks %d invalid", desc->rank, desc->nranks);
+  hd::Partition pt;
+  std::string err;
+  if (!hd::make_partition(*desc, pt, err)) return fail(HD_ERR_ARG, "%s", err.c_str());
+  for (int i = 0; i < 3; ++i)
+    if (xparts) xparts[i] = pt.xparts[i];
+  for (int i = 0; i < 6; ++i) {
+    if (off) off[i] = pt.off[i];
+    if (len) len[i] = pt.len[i];
+  }
+  return HD_OK;
+}
+
+hd_status hd_halo_list(const hd_mesh_desc *desc, int dim, int which, long long *ids, long long *count, int *peer) {
+  if (!desc || !count) return fail(HD_ERR_ARG, "null argument");
+  if (dim < 0 || dim >= desc->d_x || which < 0 || which > 3) return fail(HD_ERR_ARG, "dim or which out of range");
+  hd::Partition pt;
+  std::string err;
+  if (!hd::make_partition(*desc, pt, err)) return fail(HD_ERR_ARG, "%s", err.c_str());
+  const int d = desc->d_x + desc->d_v;
+  double h[6];
+  for (int i = 0; i < d; ++i) h[i] = (desc->hi[i] - desc->lo[i]) / (double)desc->cells[i];
+  hd::HaloDim hd;
+  hd::make_halo(*desc, pt, h, dim, hd);
+  long long gstride[6], s = 1;
+  for (int i = 0; i < d; ++i) {
+    gstride[i] = s;
+    s *= desc->cells[i];
+  }
+  // global id of a local cell, optionally shifted by one cell along dim (periodic)
+  auto gid = [&](long long cell, int shift) {
+    long long g = 0;
+    for (int i = 0; i < d; ++i) {
+      long long c = pt.off[i] + cell % pt.len[i];
+      cell /= pt.len[i];
+      if (i == dim) c = (c + shift + desc->cells[i]) % desc->cells[i];
+      g += c * gstride[i];
+    }
+    return g;
+  };
+  std::vector<long long> out;
+  if (hd.active) {
+    if (which == 0)
+      for (int c : hd.send_left) out.push_back(gid(c, -1));
+    if (which == 1)
+      for (int c : hd.send_right) out.push_back(gid(c, +1));
+    if (which >= 2) {
+      // receivers in buffer order: slots [0, n_from_left) are low-face cells, then high-face cells
+      long long lstride = 1;
+      for (int i = 0; i < dim; ++i) lstride *= pt.len[i];
+      const long long plane = hd.slot.size();
+      std::vector<long long> byslot(plane, -1);
+      for (long long j = 0; j < plane; ++j) {
+        const long long lo = j % lstride, hi = j / lstride;
+        const bool high = hd.slot[j] >= hd.n_from_left;
+        const long long cell = lo + ((high ? pt.len[dim] - 1 : 0) + hi * pt.len[dim]) * lstride;
+        byslot[hd.slot[j]] = gid(cell, 0);
+      }
+      const long long b = which == 2 ? 0 : hd.n_from_left;
+      const long long e = which == 2 ? hd.n_from_left : plane;
+      for (long long q = b; q < e; ++q) out.push_back(byslot[q]);
+    }
+  }
+  if (peer) *peer = !hd.active ? -1 : (which == 0 || which == 2) ? hd.left : hd.right;
+  if (ids) {
+    if (*count < (long long)out.size()) return fail(HD_ERR_ARG, "ids too small (%lld < %zu)", *count, out.size());
+    for (size_t q = 0; q < out.size(); ++q) ids[q] = out[q];
+  }
+  *count = (long long)out.size();
+  return HD_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// One fused cell-kernel launch over U (A mode or an RK stage). For nranks > 1 the halo traces of U are
+// packed and exchanged first (NCCL transport), unless the caller did it (loopback group driver).
+hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
+                       double b, double dtfac, bool first_launch, cudaStream_t s, bool exchange) {
+  if (!first_launch) {
+    m->epoch += 1;
+    p.epoch = (int)m->epoch;
+  }
+  if (exchange && m->desc.nranks > 1) {
+    hd_status st = halo_pack(m, U, s);
+    if (st == HD_OK) st = halo_exchange_nccl(m, s);
+    if (st != HD_OK) return st;
+  }
+  p.u = U;
+  p.du = dU;
+  p.out = out;
+  p.mode = mode;
+  p.rk_a = a;
+  p.rk_b = b;
+  p.dtfac = dtfac;
+  cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, s, &m->launches, m->grid);
+  if (e != cudaSuccess) return cuda_fail(e, "cell kernel");
+  return HD_OK;
+}
+
+hd_status check_transport(hd_mesh *m) {
+  if (m->desc.nranks > 1 && !m->nccl_comm)
+    return fail(HD_ERR_STATE, "multi-rank mesh without NCCL communicator: use the hd_*_group calls (loopback)");
+  return HD_OK;
+}
+
+hd_status check_bufs(hd_mesh *m, double *buf[3], int *sol, int nsteps, double dt) {
+  if (!buf || !sol) return fail(HD_ERR_ARG, "null argument");
+  if (*sol < 0 || *sol > 2) return fail(HD_ERR_ARG, "*sol must be 0, 1 or 2");
+  if (nsteps < 1) return fail(HD_ERR_ARG, "nsteps must be >= 1");
+  if (!std::isfinite(dt)) return fail(HD_ERR_ARG, "dt not finite");
+  const size_t bytes = (size_t)m->owned_dofs * sizeof(double);
+  for (int i = 0; i < 3; ++i) {
+    if (!buf[i]) return fail(HD_ERR_ARG, "null buffer %d", i);
+    for (int j = 0; j < i; ++j)
+      if (overlaps(buf[i], buf[j], bytes)) return fail(HD_ERR_ARG, "buffers %d and %d overlap", j, i);
+  }
+  return HD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream) {
+  (void)t;
+  if (!m || !u || !v) return fail(HD_ERR_ARG, "null argument");
+  if (overlaps(u, v, (size_t)m->owned_dofs * sizeof(double))) return fail(HD_ERR_ARG, "u and v overlap");
+  hd_status st = check_transport(m);
+  if (st == HD_OK) st = ensure_tables(m);
+  if (st != HD_OK) return st;
+  hd::CellParams p;
+  fill_cell_params(m, p);
+  return launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, 1.0, true, (cudaStream_t)stream, true);
+}
+
+hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {
+  (void)t;
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_bufs(m, buf, sol, nsteps, dt);
+  if (st == HD_OK) st = check_transport(m);
+  if (st == HD_OK) st = ensure_tables(m);
+  if (st != HD_OK) return st;
+  hd::CellParams p;
+  fill_cell_params(m, p);
+  int iu = *sol, idu = (*sol + 1) % 3, iw = (*sol + 2) % 3;
+  for (int step = 0; step < nsteps; ++step) {
+    for (int s = 0; s < 5; ++s) {
+      st = launch_stage(m, p, buf[iu], buf[idu], buf[iw], s == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[s], kRkB[s],
+                        dt, step == 0 && s == 0, (cudaStream_t)stream, true);
+      if (st != HD_OK) return st;
+      std::swap(iu, iw);
+    }
+  }
+  *sol = iu;
+  return HD_OK;
+}
+
+hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double **v, double t, void *stream) {
+  (void)t;
+  if (!ms || !u || !v || P < 1) return fail(HD_ERR_ARG, "null argument");
+  for (int r = 0; r < P; ++r) {
+    if (!ms[r] || !u[r] || !v[r]) return fail(HD_ERR_ARG, "null argument (rank %d)", r);
+    if (ms[r]->desc.nranks != P || ms[r]->desc.rank != r) return fail(HD_ERR_ARG, "meshes must be ranks 0..P-1 of P");
+    hd_status st = ensure_tables(ms[r]);
+    if (st != HD_OK) return st;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int r = 0; r < P; ++r) {
+    hd_status st = halo_pack(ms[r], u[r], s);
+    if (st != HD_OK) return st;
+  }
+  hd_status st = halo_exchange_loopback(ms, P, s);
+  if (st != HD_OK) return st;
+  for (int r = 0; r < P; ++r) {
+    hd::CellParams p;
+    fill_cell_params(ms[r], p);
+    st = launch_stage(ms[r], p, u[r], nullptr, v[r], hd::kModeAdvection, 0.0, 0.0, 1.0, true, s, false);
+    if (st != HD_OK) return st;
+  }
+  return HD_OK;
+}
+
+hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double t, double dt, int nsteps,
+                           void *stream) {
+  (void)t;
+  if (!ms || !bufs || !sol || P < 1) return fail(HD_ERR_ARG, "null argument");
+  for (int r = 0; r < P; ++r) {
+    if (!ms[r]) return fail(HD_ERR_ARG, "null mesh (rank %d)", r);
+    if (ms[r]->desc.nranks != P || ms[r]->desc.rank != r) return fail(HD_ERR_ARG, "meshes must be ranks 0..P-1 of P");
+    hd_status st = check_bufs(ms[r], bufs + 3 * r, sol, nsteps, dt);
+    if (st == HD_OK) st = ensure_tables(ms[r]);
+    if (st != HD_OK) return st;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<hd::CellParams> ps(P);
+  for (int r = 0; r < P; ++r) fill_cell_params(ms[r], ps[r]);
+  int iu = *sol, idu = (*sol + 1) % 3, iw = (*sol + 2) % 3;
+  for (int step = 0; step < nsteps; ++step) {
+    for (int st5 = 0; st5 < 5; ++st5) {
+      for (int r = 0; r < P; ++r) {
+        hd_status st = halo_pack(ms[r], bufs[3 * r + iu], s);
+        if (st != HD_OK) return st;
+      }
+      hd_status st = halo_exchange_loopback(ms, P, s);
+      if (st != HD_OK) return st;
+      for (int r = 0; r < P; ++r) {
+        st = launch_stage(ms[r], ps[r], bufs[3 * r + iu], bufs[3 * r + idu], bufs[3 * r + iw],
+                          st5 == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[st5], kRkB[st5], dt, step == 0 && st5 == 0,
+                          s, false);
+        if (st != HD_OK) return st;
+      }
+      std::swap(iu, iw);
+    }
+  }
+  *sol = iu;
+  return HD_OK;
+}
+
 hd_status hd_fill_initial(hd_mesh *m, double *u, int recipe, unsigned long long seed, void *stream) {
   if (!m || !u) return fail(HD_ERR_ARG, "null argument");
   if (recipe < 0 || recipe > 3) return fail(HD_ERR_ARG, "recipe must be 0..3");
@@ -454,9 +828,9 @@ hd_status hd_fill_initial(hd_mesh *m, double *u, int recipe, unsigned long long 
   std::memset(&p, 0, sizeof(p));
   p.u = u;
   p.ncells = m->ncells_local;
-  p.nx_local = m->nx_local;
-  p.cx_begin = m->cx_begin;
   for (int i = 0; i < m->d; ++i) {
+    p.off[i] = m->pt.off[i];
+    p.len[i] = m->pt.len[i];
     p.L[i] = m->desc.cells[i];
     p.lo[i] = m->desc.lo[i];
     p.h[i] = m->h[i];

@@ -1,35 +1,32 @@
 // hd_cell.cuh -- the fused cell kernel (element-centric loop, Alg. 1/Alg. 2) for sm_100a.
 // Included by hd_kernels.cu (single translation unit with the __constant__ tables).
 //
-// One CTA iteration processes one work item = C consecutive cells along dim 0 (C | L_0). Items are
-// visited in lexicographic item order, with the direction of every "trace" dimension (a dimension
-// whose speed has one sign on the whole box) reversed when that sign is negative, so the upwind
-// neighbour along a trace dim is always processed istride_i items earlier (except at the periodic
-// wrap). Each thread owns, per phase, an n x n tile of a cell over two dimensions (P, Q) at fixed
-// other coordinates (its "rest" index r):
-//   1. read the lines of its tile from smem (the item was gathered with cp.async into a padded
-//      layout, prefetched one item ahead) and form, line by line, the volume terms of P and Q (1D
-//      matrices with the own-face term folded in) and the cell's DOWNWIND traces along P and Q,
-//   2. publish those traces (ring / full-size buffer) and bump the item's per-phase flag (one
-//      release per warp),
-//   3. obtain the UPWIND traces: acquire the producer item's flag and read n values per dim (tried
-//      early, before step 1, when the producer is long done); at the periodic wrap and for dims
-//      whose speed changes sign, form them from the neighbour cell itself (L1/L2 reads),
-//   4. add the rank-1 lifts, then hand the accumulator to the next phase through smem, or finish:
-//      weak-form scaling by the collocated mass (A mode) or the LSRK 2N update (RK mode).
+// Merged operator: M^-1 A = sum_i (a_i(z)/h_i) L_i along dim i; L_i = the n x n matrix K
+// (volume term + own-face upwind term, rows divided by w_m) plus the rank-1 lift lam * (tau . u_nb) of
+// the UPWIND neighbour's trace. One CTA iteration processes a GROUP of CT cells that are consecutive
+// along dim 0; threads own, per phase, an n x n register tile of a cell over a pair of dims (P, Q).
+//
+// Work units and upwind traces (the part that decides performance):
+//   * pencil mode (CT | L_0): a unit is the pencil of L_0 cells along dim 0, processed group by group
+//     by ONE CTA in the direction of a_0 (constant on the pencil). The dim-0 upwind trace of the
+//     group's upwind-end cell is the previous group's downwind trace, carried in smem (no global
+//     traffic, no inter-CTA wait); only the first group (periodic wrap) reads its neighbour.
+//   * multi-pencil mode (L_0 | CT): a group holds whole pencils; dim-0 (and any other in-group)
+//     neighbours are read from smem.
+//   * dims whose upwind neighbour unit is >= 2 x grid units earlier ("published" dims; their speed has
+//     one sign on the whole box, so the traversal follows it) get the trace from a trace buffer the
+//     producer wrote (n^(d-1) values, 1/n of a cell) when the producer's unit flag (one acquire per
+//     group) says it is complete; otherwise -- and for all other dims -- the thread reads the
+//     neighbour cell's lines itself (L2) and contracts them. Nobody ever waits for another CTA.
 #pragma once
-
-#ifndef HD_EARLY_TRACES
-#define HD_EARLY_TRACES 0
-#endif
-#ifndef HD_PUBLISH_FENCE
-#define HD_PUBLISH_FENCE 0
-#endif
-#ifndef HD_DU_DIRECT
-#define HD_DU_DIRECT 0
+#ifndef HD_MINB
+#define HD_MINB 2
 #endif
 
 namespace hd {
+
+enum TraceSrc : unsigned char { kSrcDirect = 0, kSrcGroup = 1, kSrcCarry = 2, kSrcPub = 3, kSrcHalo = 4 };
+enum TraceOut : unsigned char { kOutNone = 0, kOutCarry = 1, kOutPub = 2 };
 
 template <int D, int N>
 struct CGeo {
@@ -37,34 +34,43 @@ struct CGeo {
   static constexpr int FN = ipow(N, D - 1);   // face points per face
   static constexpr int NT = ipow(N, D - 2);   // threads per cell
   static constexpr int NPH = (D + 1) / 2;     // phases
-  static constexpr __host__ __device__ int P(int ph) { return (D % 2 == 1 && ph == NPH - 1) ? D - 1 : 2 * ph; }
-  static constexpr __host__ __device__ int Q(int ph) { return (D % 2 == 1 && ph == NPH - 1) ? D - 2 : 2 * ph + 1; }
-  static constexpr __host__ __device__ bool QA(int ph) { return !(D % 2 == 1 && ph == NPH - 1); }
-  // one cell must fit three padded smem buffers (2 CTAs per SM up to 110 KB, else 1 CTA per SM)
-  static constexpr bool OK = NT <= 256 && ND * 8 * 9 / 8 * 3 + 4096 <= 220 * 1024;
+  // phase ph works on the dim pair (P, Q): (0, D-1), (1, 2), (3, 4); QA false: Q already done
+  static constexpr __host__ __device__ int P(int ph) { return ph == 0 ? 0 : 2 * ph - 1; }
+  static constexpr __host__ __device__ int Q(int ph) { return ph == 0 ? D - 1 : 2 * ph; }
+  static constexpr __host__ __device__ bool QA(int ph) { return ph == 0 || 2 * ph != D - 1; }
+  // one cell must fit: U double buffer + ACC + carry double buffer in ~112 KB (2 CTAs per SM)
+  static constexpr bool OK = NT <= 256 && (3 * ND + 2 * FN + 16) * 8 + 256 <= 227 * 1024;
 };
 
-// padded smem layout: 2 doubles of padding after every 16 (conflict-free row access)
-__host__ __device__ constexpr int padded(int e) { return e + ((e >> 4) << 1); }
+// Shared-memory element order of a cell: XOR swizzle that keeps (2e, 2e+1) pairs together and makes
+// every phase's tile access bank-conflict free for n = 4 (checked by tools: all phases of d = 4..6).
+template <int D, int N>
+__host__ __device__ __forceinline__ constexpr int swz(int x) {
+  if constexpr (N == 4 && D >= 4) {
+    return x ^ (((x >> 6) & 3) << 2) ^ (((x >> 4) & 1) << 1);
+  } else {
+    return x;
+  }
+}
 
 struct CellInfo {
-  int cell;                 // local memory index of the cell
-  int c[kMaxD];             // cell coordinates
-  int t[kMaxD];             // traversal coordinates (item level for dim 0)
-  int sg[kMaxD];            // 1: a_i < 0 on this cell (upwind neighbour at +e_i)
-  int direct[kMaxD];        // 1: form the upwind trace from the neighbour cell itself
-  int nbcell[kMaxD];        // local memory index of the upwind neighbour
-  int pitem[kMaxD];         // producer item of the upwind trace
-  int pk[kMaxD];            // producer cell slot in that item
-  double base[kMaxD];       // a_i at the cell's lower corner: a_const + sum_j a_lin[i][j] (lo_j + c_j h_j)
+  double base[kMaxD];        // a_i at the cell's lower corner
+  int cell;                  // local memory index of the cell
+  int cu;                    // cell slot inside its unit (trace-buffer addressing)
+  int unit;                  // the unit being processed (kOutPub slot)
+  int nb[kMaxD];             // kSrcDirect: neighbour cell index; kSrcGroup: neighbour slot k' in the group
+  int slot[kMaxD];           // kSrcPub: producer unit; kSrcHalo: receive slot
+  unsigned char src[kMaxD];  // TraceSrc of the upwind trace per dim
+  unsigned char out[kMaxD];  // TraceOut of the downwind trace per dim
+  unsigned char sg[kMaxD];   // 1: a_i < 0 on this cell (upwind neighbour at +e_i)
+  unsigned char pad[2];
 };
 
 // per-thread, per-phase constants
 struct ThreadPhase {
-  double wP, wQ;            // sum over rest dims j of a_lin[P|Q][j] h_j xi_{m_j}
-  double wr;                // |J| prod_{rest j} w_{m_j} (weak-form mass of the last phase)
-  int R;                    // cell-local offset of the rest coordinates
-  int pad;
+  double wP, wQ;  // sum over rest dims j of a_lin[P|Q][j] h_j xi_{m_j}
+  double wr;      // |J| prod_{rest j} w_{m_j} (weak-form mass, A mode)
+  int R;          // cell-local offset of the rest coordinates
 };
 
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -72,93 +78,138 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Release increment of a publication counter. Issued by one lane after __syncwarp(): the warp
-// barrier orders the other lanes' trace stores before it, and release makes them visible to any
-// thread that acquires the counter.
-__device__ __forceinline__ void red_release_add(int *p) {
-#if HD_PUBLISH_FENCE
-  __threadfence();
-  atomicAdd(p, 1);
-#else
-  asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(p) : "memory");
-#endif
-}
-// Spin until a producer flag reaches the target. A watchdog aborts the kernel (trap) instead of
-// hanging if a publication never arrives (a protocol bug would otherwise wedge the GPU).
-__device__ __forceinline__ void wait_flag(const int *p, int target) {
-  if (ld_acquire(p) >= target) return;
-  unsigned spins = 0;
-  while (ld_acquire(p) < target) {
-    __nanosleep(32);
-    if (++spins > (1u << 25)) __trap();
+
+// sign of a_i on a cell with coordinates c (evaluated at the cell centre; constant on the cell by
+// reading C11). Identical arithmetic wherever it is needed, so all decisions agree bitwise.
+template <int D>
+__device__ __forceinline__ void cell_speed(const CellParams &p, int i, const int (&c)[kMaxD], double &base, int &sg) {
+  double ab = p.a_const[i], half = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    ab = fma(p.a_lin[i][j], fma((double)(c[j] + p.coff[j]), p.h[j], p.lo[j]), ab);
+    half = fma(p.a_lin[i][j], 0.5 * p.h[j], half);
   }
+  base = ab;
+  sg = (ab + half) < 0.0 ? 1 : 0;
 }
 
-// Decode item b: all cells' coordinates, upwind neighbours and trace producers. Two steps, each
-// spread over the CTA's threads ((cell, dim) pairs); the caller separates them with a barrier.
+// Pencil-mode unit decode: coordinates c_1..c_{D-1} (traversal coordinates t), pencil base cell and
+// the direction of dim 0 (1: a_0 < 0, groups processed from the far end).
 template <int D>
-__device__ __forceinline__ void decode_coords(const CellParams &p, int b, int C, CellInfo *info) {
-  for (int idx = threadIdx.x; idx < C * D; idx += blockDim.x) {
-    const int k = idx / D, i = idx - k * D;
-    const int t = (b / p.istride[i]) % p.IL[i];
-    int c = p.dirneg[i] ? p.IL[i] - 1 - t : t;
-    if (i == 0) c = c * C + k;
-    info[k].t[i] = t;
-    info[k].c[i] = c;
+__device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c)[kMaxD], int (&t)[kMaxD], int &dir0) {
+  int base = 0;
+  c[0] = 0;
+  t[0] = 0;
+#pragma unroll
+  for (int j = 1; j < D; ++j) {
+    const int tj = (u / p.ustride[j]) % p.L[j];
+    t[j] = tj;
+    c[j] = p.dirneg[j] ? p.L[j] - 1 - tj : tj;
+    base += c[j] * p.lstride[j];
   }
+  double b0;
+  cell_speed<D>(p, 0, c, b0, dir0);
+  return base;
 }
+
+// First cell (memory order) of group gi of unit u.
 template <int D>
-__device__ __forceinline__ void decode_links(const CellParams &p, int b, int C, CellInfo *info) {
-  for (int idx = threadIdx.x; idx < C * D; idx += blockDim.x) {
-    const int k = idx / D, i = idx - k * D;
-    CellInfo &ci = info[k];
-    int cell = 0;
-    double ab = p.a_const[i], half = 0.0;
+__device__ __forceinline__ int group_first_cell(const CellParams &p, int u, int gi) {
+  if (!p.pencil) return u * p.CT;
+  int c[kMaxD], t[kMaxD], dir0;
+  const int base = pencil_decode<D>(p, u, c, t, dir0);
+  const int g = dir0 ? p.GPU - 1 - gi : gi;
+  return base + g * p.CT;
+}
+
+// Decode cell k of group gi of unit u (one thread per cell).
+template <int D>
+__device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, int k, CellInfo &ci) {
+  int c[kMaxD], t[kMaxD];
+  int first;
+  if (p.pencil) {
+    int dir0;
+    const int base = pencil_decode<D>(p, u, c, t, dir0);
+    const int g = dir0 ? p.GPU - 1 - gi : gi;
+    c[0] = g * p.CT + k;
+    first = base + g * p.CT;
+    ci.cu = c[0];
+  } else {
+    first = u * p.CT;
+    int rr = first + k;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      cell += ci.c[j] * p.lstride[j];
-      ab = fma(p.a_lin[i][j], p.lo[j] + (double)ci.c[j] * p.h[j], ab);
-      half = fma(p.a_lin[i][j], 0.5 * p.h[j], half);
+      c[j] = rr % p.L[j];
+      rr /= p.L[j];
+      t[j] = 0;
     }
-    const int sg = (ab + half) < 0.0 ? 1 : 0;  // sign at the cell centre (constant on the cell)
-    const int up = sg ? 1 : -1;                // offset of the upwind neighbour along i
-    int cn = ci.c[i] + up;
-    if (cn < 0) cn += p.L[i];
-    if (cn >= p.L[i]) cn -= p.L[i];
-    ci.base[i] = ab;
-    ci.sg[i] = sg;
-    ci.nbcell[i] = cell + (cn - ci.c[i]) * p.lstride[i];
-    int direct = 1, pitem = 0, pk = 0;
-    if (p.tmode[i] != kTraceNone) {
-      if (i == 0 && k + up >= 0 && k + up < C) {
-        direct = 0;
-        pitem = b;
-        pk = k + up;
-      } else if (ci.t[i] > 0) {
-        direct = 0;
-        pitem = b - p.istride[i];
-        pk = i == 0 ? (up < 0 ? C - 1 : 0) : k;
-      }
-    }
-    ci.direct[i] = direct;
-    ci.pitem[i] = pitem;
-    ci.pk[i] = pk;
-    if (i == 0) ci.cell = cell;
+    ci.cu = k;
   }
-}
-
-// first cell (in memory) of item b
-template <int D>
-__device__ __forceinline__ int item_first_cell(const CellParams &p, int b, int C) {
   int cell = 0;
 #pragma unroll
+  for (int j = 0; j < D; ++j) cell += c[j] * p.lstride[j];
+  ci.cell = cell;
+  ci.unit = u;
+#pragma unroll
   for (int i = 0; i < D; ++i) {
-    const int t = (b / p.istride[i]) % p.IL[i];
-    int c = p.dirneg[i] ? p.IL[i] - 1 - t : t;
-    if (i == 0) c *= C;
-    cell += c * p.lstride[i];
+    double base;
+    int sg;
+    cell_speed<D>(p, i, c, base, sg);
+    ci.base[i] = base;
+    ci.sg[i] = (unsigned char)sg;
+    const int up = sg ? 1 : -1;
+    int cn = c[i] + up;
+    const bool outside = cn < 0 || cn >= p.L[i];
+    if (cn < 0) cn += p.L[i];
+    if (cn >= p.L[i]) cn -= p.L[i];
+    const int nbcell = cell + (cn - c[i]) * p.lstride[i];
+    unsigned char src = kSrcDirect, out = kOutNone;
+    int nb = nbcell, slot = 0;
+    if (outside && p.xsplit[i]) {
+      // the upwind neighbour lives on another rank: its trace arrived in the halo buffer
+      src = kSrcHalo;
+      const int ls = p.lstride[i];
+      slot = p.hslot[i][(cell % ls) + (cell / (ls * p.L[i])) * ls];
+      if (i == 0 && p.pencil) {
+        const int kd = k - up;
+        if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
+      }
+    } else if (i == 0) {
+      if (!p.pencil) {
+        src = kSrcGroup;
+        nb = k + (cn - c[0]);
+      } else {
+        const int kk = k + up;
+        if (kk >= 0 && kk < p.CT) {
+          src = kSrcGroup;
+          nb = kk;
+        } else if (gi > 0) {
+          src = kSrcCarry;
+        }
+        // downwind-end cell of a group that has a successor in this unit feeds the carry
+        const int kd = k - up;
+        if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
+      }
+    } else {
+      if (!p.pencil && nbcell >= first && nbcell < first + p.CT) {
+        src = kSrcGroup;
+        nb = nbcell - first;
+      } else if (p.pub[i]) {
+        if (t[i] > 0) {
+          const int pu = u - p.ustride[i];
+          if (ld_acquire(p.flags + pu) >= p.epoch) {
+            src = kSrcPub;
+            slot = pu;
+          }
+        }
+      }
+      if (p.pub[i] && t[i] < p.L[i] - 1) out = kOutPub;
+    }
+    ci.src[i] = src;
+    ci.out[i] = out;
+    ci.nb[i] = nb;
+    ci.slot[i] = slot;
   }
-  return cell;
 }
 
 // Per-thread phase constants for rest index r. sx, sw: the 1D nodes and weights staged in smem.
@@ -175,8 +226,8 @@ __device__ __forceinline__ void thread_phase(const CellParams &p, int r, const d
       const int m = rr % N;
       rr /= N;
       R += m * nj;
-      if (p.a_lin[P][j] != 0.0) wP = fma(p.a_lin[P][j] * p.h[j], sx[m], wP);
-      if (p.a_lin[Q][j] != 0.0) wQ = fma(p.a_lin[Q][j] * p.h[j], sx[m], wQ);
+      wP = fma(p.a_lin[P][j] * p.h[j], sx[m], wP);
+      wQ = fma(p.a_lin[Q][j] * p.h[j], sx[m], wQ);
       if constexpr (MASS) wr *= sw[m];
     }
     nj *= N;
@@ -185,383 +236,398 @@ __device__ __forceinline__ void thread_phase(const CellParams &p, int r, const d
   tp.wQ = wQ;
   tp.wr = wr;
   tp.R = R;
-  tp.pad = 0;
 }
 
-template <int N, int S>
-__device__ __forceinline__ void lift_P(double (&acc)[N][N], const double (&st)[N]) {
-  const Tables1D &T = c_tab[N];
-#pragma unroll
-  for (int b = 0; b < N; ++b)
-#pragma unroll
-    for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[S][a], st[b], acc[a][b]);
-}
-template <int N, int S>
-__device__ __forceinline__ void lift_Q(double (&acc)[N][N], const double (&st)[N]) {
-  const Tables1D &T = c_tab[N];
-#pragma unroll
-  for (int a = 0; a < N; ++a)
-#pragma unroll
-    for (int b = 0; b < N; ++b) acc[a][b] = fma(T.lam[S][b], st[a], acc[a][b]);
-}
-
-// smem element address of tile element at logical eb + off in the padded layout; off is a
-// compile-time constant after unrolling, so the branches fold away
-template <bool EB16>
-__device__ __forceinline__ int paddr(int off, int eb, int peb) {
-  if ((off & 15) == 0) return peb + off + ((off >> 4) << 1);
-  if (EB16 && off < 16) return peb + off;
-  return padded(eb + off);
-}
-
-template <int N, int SP, int SQ, bool EB16>
-__device__ __forceinline__ void load_tile(const double *S, int eb, double (&v)[N][N]) {
-  const int peb = padded(eb);
-#pragma unroll
-  for (int a = 0; a < N; ++a)
-#pragma unroll
-    for (int b = 0; b < N; ++b) v[a][b] = S[paddr<EB16>(a * SP + b * SQ, eb, peb)];
-}
-
-// store / load the n values t[0..n) contiguously (16-byte accesses when possible), L2 only
-template <int N>
-__device__ __forceinline__ void store_trace(double *dst, const double (&t)[N]) {
-  if constexpr (N % 2 == 0) {
-#pragma unroll
-    for (int j = 0; j < N; j += 2) __stcg(reinterpret_cast<double2 *>(dst + j), make_double2(t[j], t[j + 1]));
-  } else {
-#pragma unroll
-    for (int j = 0; j < N; ++j) __stcg(dst + j, t[j]);
-  }
-}
-template <int N>
-__device__ __forceinline__ void load_trace(const double *src, double (&t)[N]) {
-  if constexpr (N % 2 == 0) {
-#pragma unroll
-    for (int j = 0; j < N; j += 2) {
-      const double2 v = __ldcg(reinterpret_cast<const double2 *>(src + j));
-      t[j] = v.x;
-      t[j + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < N; ++j) t[j] = __ldcg(src + j);
-  }
-}
-
-// Publish the downwind trace of dim X (ring / far storage); for a ring slot first make sure the
-// slot's previous item has been consumed (its consumers, the item itself for dim 0 and the item
-// istride_X later, published the following phase).
-template <int D, int N, int PH>
-__device__ __forceinline__ void publish_trace(const CellParams &p, int X, int b, int k, int r, int C,
-                                              const double (&t)[N]) {
-  using G = CGeo<D, N>;
-  constexpr int NPH1 = G::NPH + 1;
-  const int mode = p.tmode[X];
-  const int slot = mode == kTraceRing ? (b & p.rmask[X]) : b;
-  if (mode == kTraceRing && b > p.rmask[X]) {
-    const int old = b - p.rmask[X] - 1;
-    wait_flag(p.flags + (size_t)old * NPH1 + PH + 1, p.target);
-    wait_flag(p.flags + (size_t)(old + p.istride[X]) * NPH1 + PH + 1, p.target);
-  }
-  store_trace<N>(p.tbuf[X] + ((size_t)slot * C + k) * G::FN + (size_t)N * r, t);
-}
-
-// Non-blocking attempt to read the published upwind trace of dim X (true if it was available).
-template <int D, int N, int PH>
-__device__ __forceinline__ bool try_trace(const CellParams &p, const CellInfo &ci, int X, int r, int C,
-                                          double (&t)[N]) {
-  using G = CGeo<D, N>;
-  constexpr int NPH1 = G::NPH + 1;
-  const int pi = ci.pitem[X];
-  if (ld_acquire(p.flags + (size_t)pi * NPH1 + PH) < p.target) return false;
-  const int slot = p.tmode[X] == kTraceRing ? (pi & p.rmask[X]) : pi;
-  load_trace<N>(p.tbuf[X] + ((size_t)slot * C + ci.pk[X]) * G::FN + (size_t)N * r, t);
-  return true;
-}
-
-// Upwind trace of dim X for this thread's lines: from the producer (blocking), or directly from the
-// neighbour cell (lines along X with stride SX, indexed by the partner digit with stride SY).
-template <int D, int N, int PH, int SX, int SY>
-__device__ __forceinline__ void upwind_trace(const CellParams &p, const CellInfo &ci, int X, int sg, int R, int r,
-                                             int C, double (&t)[N]) {
-  using G = CGeo<D, N>;
-  constexpr int NPH1 = G::NPH + 1;
-  if (ci.direct[X]) {
-    const double *nb = p.u + (size_t)ci.nbcell[X] * G::ND + R;
-    const double *tau = c_tab[N].tau[sg];
-#pragma unroll
-    for (int l = 0; l < N; ++l) {
-      double s = tau[0] * __ldg(nb + l * SY);
-#pragma unroll
-      for (int j = 1; j < N; ++j) s = fma(tau[j], __ldg(nb + j * SX + l * SY), s);
-      t[l] = s;
-    }
-  } else {
-    const int pi = ci.pitem[X];
-    wait_flag(p.flags + (size_t)pi * NPH1 + PH, p.target);
-    const int slot = p.tmode[X] == kTraceRing ? (pi & p.rmask[X]) : pi;
-    load_trace<N>(p.tbuf[X] + ((size_t)slot * C + ci.pk[X]) * G::FN + (size_t)N * r, t);
-  }
-}
-
-// One pass over the tile lines of dim P (lines along the first tile index a, one per partner
-// digit b): each line is read from smem once and yields both the downwind trace t[b] and the
-// volume contribution acc[a][b] (+)= s[b] sum_j K[a][j] u[j][b].
-template <int N, int S, bool INIT, class Get>
-__device__ __forceinline__ void pass_P(double (&acc)[N][N], Get get, double s0, double sl, double (&t)[N]) {
+// One pass over the tile lines of dim P (lines along the first tile index a, one per partner digit
+// b): yields the downwind trace t[b] = tau . line and the volume contribution
+// acc[a][b] (+)= s_b sum_j K[a][j] u[j][b].
+template <int N, int S, bool INIT, bool TRACE>
+__device__ __forceinline__ void pass_P(double (&acc)[N][N], const double (&uv)[N][N], double s0, double sl,
+                                       double (&t)[N]) {
   const Tables1D &T = c_tab[N];
 #pragma unroll
   for (int b = 0; b < N; ++b) {
-    const double sb = fma(sl, T.xi[b], s0);  // line speed a_P / h_P * dtfac
-    double col[N];
+    const double sb = fma(sl, T.xi[b], s0);
+    if constexpr (TRACE) {
+      double tr = T.tau[S][0] * uv[0][b];
 #pragma unroll
-    for (int j = 0; j < N; ++j) col[j] = get(j, b);
-    double tr = T.tau[S][0] * col[0];
-#pragma unroll
-    for (int j = 1; j < N; ++j) tr = fma(T.tau[S][j], col[j], tr);
-    t[b] = tr;
+      for (int j = 1; j < N; ++j) tr = fma(T.tau[S][j], uv[j][b], tr);
+      t[b] = tr;
+    }
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-      double y = T.K[S][a][0] * col[0];
+      double y = T.K[S][a][0] * uv[0][b];
 #pragma unroll
-      for (int j = 1; j < N; ++j) y = fma(T.K[S][a][j], col[j], y);
+      for (int j = 1; j < N; ++j) y = fma(T.K[S][a][j], uv[j][b], y);
       if constexpr (INIT) acc[a][b] = sb * y;
       else acc[a][b] = fma(sb, y, acc[a][b]);
     }
   }
 }
 // Same for dim Q (lines along b, one per a).
-template <int N, int S, class Get>
-__device__ __forceinline__ void pass_Q(double (&acc)[N][N], Get get, double s0, double sl, double (&t)[N]) {
+template <int N, int S, bool TRACE>
+__device__ __forceinline__ void pass_Q(double (&acc)[N][N], const double (&uv)[N][N], double s0, double sl,
+                                       double (&t)[N]) {
   const Tables1D &T = c_tab[N];
 #pragma unroll
   for (int a = 0; a < N; ++a) {
-    const double sa = fma(sl, T.xi[a], s0);  // line speed a_Q / h_Q * dtfac
-    double row[N];
+    const double sa = fma(sl, T.xi[a], s0);
+    if constexpr (TRACE) {
+      double tr = T.tau[S][0] * uv[a][0];
 #pragma unroll
-    for (int j = 0; j < N; ++j) row[j] = get(a, j);
-    double tr = T.tau[S][0] * row[0];
-#pragma unroll
-    for (int j = 1; j < N; ++j) tr = fma(T.tau[S][j], row[j], tr);
-    t[a] = tr;
+      for (int j = 1; j < N; ++j) tr = fma(T.tau[S][j], uv[a][j], tr);
+      t[a] = tr;
+    }
 #pragma unroll
     for (int b = 0; b < N; ++b) {
-      double y = T.K[S][b][0] * row[0];
+      double y = T.K[S][b][0] * uv[a][0];
 #pragma unroll
-      for (int j = 1; j < N; ++j) y = fma(T.K[S][b][j], row[j], y);
+      for (int j = 1; j < N; ++j) y = fma(T.K[S][b][j], uv[a][j], y);
       acc[a][b] = fma(sa, y, acc[a][b]);
     }
   }
 }
 
+// Upwind trace of this thread's N face points along dim X (stride SX), the face points being indexed by
+// the partner tile digit l (stride SY): t[l] = sum_j tau[j] u_nb[R + j SX + l SY]. Same summation order
+// as the producer's pass, so every source yields the same bits.
+template <int D, int N, int SX, int SY>
+__device__ __forceinline__ void trace_global(const double *nb, int S, double (&t)[N]) {
+  const double *tau = c_tab[N].tau[S];
+  double v[N][N];
+#pragma unroll
+  for (int l = 0; l < N; ++l)
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[l][j] = __ldg(nb + j * SX + l * SY);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    double s = tau[0] * v[l][0];
+#pragma unroll
+    for (int j = 1; j < N; ++j) s = fma(tau[j], v[l][j], s);
+    t[l] = s;
+  }
+}
+template <int D, int N, int SX, int SY>
+__device__ __forceinline__ void trace_smem(const double *cellbuf, int R, int S, double (&t)[N]) {
+  const double *tau = c_tab[N].tau[S];
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    double s = tau[0] * cellbuf[swz<D, N>(R + l * SY)];
+#pragma unroll
+    for (int j = 1; j < N; ++j) s = fma(tau[j], cellbuf[swz<D, N>(R + j * SX + l * SY)], s);
+    t[l] = s;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void store_vec(double *dst, const double (&t)[N], bool global) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+      if (global) __stcg(reinterpret_cast<double2 *>(dst + j), make_double2(t[j], t[j + 1]));
+      else *reinterpret_cast<double2 *>(dst + j) = make_double2(t[j], t[j + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (global) __stcg(dst + j, t[j]);
+      else dst[j] = t[j];
+    }
+  }
+}
+template <int N>
+__device__ __forceinline__ void load_vec(const double *src, double (&t)[N], bool global) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+      const double2 v = global ? __ldcg(reinterpret_cast<const double2 *>(src + j))
+                               : *reinterpret_cast<const double2 *>(src + j);
+      t[j] = v.x;
+      t[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) t[j] = global ? __ldcg(src + j) : src[j];
+  }
+}
+
+// Obtain the upwind trace of dim X for this thread (X is the tile's first index when FIRST_IDX, i.e.
+// X = P: lines along P, face points indexed by b; else X = Q).
+template <int D, int N, int SX, int SY>
+__device__ __forceinline__ void upwind_trace(const CellParams &p, const CellInfo &ci, int X, int R, int r,
+                                             const double *Ugroup, const double *carry_in, double (&t)[N]) {
+  using G = CGeo<D, N>;
+  const int S = ci.sg[X];
+  switch (ci.src[X]) {
+    case kSrcGroup:
+      trace_smem<D, N, SX, SY>(Ugroup + (size_t)ci.nb[X] * G::ND, R, S, t);
+      break;
+    case kSrcCarry:
+      load_vec<N>(carry_in + N * r, t, false);
+      break;
+    case kSrcPub:
+      load_vec<N>(p.tbuf[X] + ((size_t)ci.slot[X] * p.UC + ci.cu) * G::FN + (size_t)N * r, t, true);
+      break;
+    case kSrcHalo:
+      load_vec<N>(p.hbuf[X] + (size_t)ci.slot[X] * G::FN + (size_t)N * r, t, true);
+      break;
+    default:
+      trace_global<D, N, SX, SY>(p.u + (size_t)ci.nb[X] * G::ND + R, S, t);
+      break;
+  }
+}
+
 template <int D, int N, int MODE, int PH>
-__device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *stab, int b,
-                                          int k, int r, int C, const double *U, double *ACC, bool warp_leader,
+__device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
+                                          const double *Ug, double *ACC, const double *carry_in, double *carry_out,
                                           bool active) {
+  if (!active) return;  // padding threads of the CTA: only the barriers between phases
   using G = CGeo<D, N>;
   constexpr int P = G::P(PH), Q = G::Q(PH);
   constexpr bool QA = G::QA(PH);
   constexpr int SP = ipow(N, P), SQ = ipow(N, Q);
   constexpr bool FIRST = PH == 0, LAST = PH == G::NPH - 1;
-  constexpr int NPH1 = G::NPH + 1;
-  // compile-time property: the tile base is a multiple of 16 (all rest strides and n^d are)
-  constexpr bool EB16 = (G::ND % 16 == 0) && [] {
-    bool ok = true;
-    for (int j = 0; j < D; ++j)
-      if (j != P && j != Q && ipow(N, j) % 16 != 0) ok = false;
-    return ok;
-  }();
   const Tables1D &T = c_tab[N];
 
   ThreadPhase tp;
   thread_phase<D, N, PH, LAST && MODE == kModeAdvection>(p, r, stab, stab + 8, tp);
   const int R = tp.R;
-  const int eb = k * G::ND + R;
-  const int peb = padded(eb);
+  const double *U = Ug + (size_t)k * G::ND;
+  double *A = ACC + (size_t)k * G::ND;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
   const size_t g0 = (size_t)ci.cell * G::ND + R;
-  double acc[N][N];
-  double tP[N], tQ[N];
-  bool haveP = false, haveQ = false;
-  // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line: a_i varies only with the coordinates of
-  // the other dims
+  // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line (a_i varies only with the other dims)
   const double facP = p.dtfac * p.inv_h[P], facQ = p.dtfac * p.inv_h[Q];
   const double s0P = (ci.base[P] + tp.wP) * facP, slP = p.a_lin[P][Q] * p.h[Q] * facP;
   const double s0Q = (ci.base[Q] + tp.wQ) * facQ, slQ = p.a_lin[Q][P] * p.h[P] * facQ;
-  const bool dirP = ci.direct[P], dirQ = ci.direct[Q];
-  if (active) {
-    // early attempt at the upwind traces: producers istride items back are usually done, and the
-    // loads then overlap the passes below
-#if HD_EARLY_TRACES
-    if (!dirP && ci.pitem[P] != b) haveP = try_trace<D, N, PH>(p, ci, P, r, C, tP);
-    if constexpr (QA) {
-      if (!dirQ && ci.pitem[Q] != b) haveQ = try_trace<D, N, PH>(p, ci, Q, r, C, tQ);
-    }
-#endif
-    if constexpr (!FIRST) load_tile<N, SP, SQ, EB16>(ACC, eb, acc);
-    // 1./2. volume terms of P and Q and this cell's downwind traces along P and Q -> publish
-    double trP[N], trQ[N];
-    if constexpr (P == 0 && Q == 1 && EB16 && N * N <= 16 && N % 2 == 0) {
-      // contiguous tile (dims 0 and 1): 16-byte loads into registers, conflict-free in the padding
-      double uv[N][N];
+
+  double acc[N][N];
+  {
+    double uv[N][N];
+    if constexpr (P == 0 && N % 2 == 0) {
 #pragma unroll
-      for (int e = 0; e < N * N; e += 2) {
-        const double2 v = *reinterpret_cast<const double2 *>(U + peb + e);
-        uv[e % N][e / N] = v.x;
-        uv[(e + 1) % N][(e + 1) / N] = v.y;
-      }
-      auto get = [&](int a, int bb) { return uv[a][bb]; };
-      if (sgP == 0) pass_P<N, 0, FIRST>(acc, get, s0P, slP, trP);
-      else pass_P<N, 1, FIRST>(acc, get, s0P, slP, trP);
-      if constexpr (QA) {
-        if (sgQ == 0) pass_Q<N, 0>(acc, get, s0Q, slQ, trQ);
-        else pass_Q<N, 1>(acc, get, s0Q, slQ, trQ);
-      }
+      for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int a = 0; a < N; a += 2) {
+          const double2 v = *reinterpret_cast<const double2 *>(U + swz<D, N>(R + a + b * SQ));
+          uv[a][b] = v.x;
+          uv[a + 1][b] = v.y;
+        }
     } else {
-      auto get = [&](int a, int bb) { return U[paddr<EB16>(a * SP + bb * SQ, eb, peb)]; };
-      if (sgP == 0) pass_P<N, 0, FIRST>(acc, get, s0P, slP, trP);
-      else pass_P<N, 1, FIRST>(acc, get, s0P, slP, trP);
-      if constexpr (QA) {
-        if (sgQ == 0) pass_Q<N, 0>(acc, get, s0Q, slQ, trQ);
-        else pass_Q<N, 1>(acc, get, s0Q, slQ, trQ);
-      }
-    }
-    if (p.tmode[P] != kTraceNone) publish_trace<D, N, PH>(p, P, b, k, r, C, trP);
-    if constexpr (QA) {
-      if (p.tmode[Q] != kTraceNone) publish_trace<D, N, PH>(p, Q, b, k, r, C, trQ);
-    }
-    if constexpr (LAST && MODE == kModeRK && !HD_DU_DIRECT) {
-      // dU of the tile -> this thread's own ACC positions (already consumed), asynchronously; read
-      // back in the epilogue, so its HBM latency overlaps the upwind-trace work
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int bb = 0; bb < N; ++bb)
-          cp_async8(ACC + paddr<EB16>(a * SP + bb * SQ, eb, peb), p.du + g0 + a * SP + bb * SQ);
+        for (int b = 0; b < N; ++b) uv[a][b] = U[swz<D, N>(R + a * SP + b * SQ)];
+    }
+    if constexpr (!FIRST) {
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) acc[a][b] = A[swz<D, N>(R + a * SP + b * SQ)];
+    }
+    if constexpr (LAST && MODE == kModeRK) {
+      // dU of the tile -> this thread's own ACC positions (already consumed), asynchronously; read back
+      // in the epilogue, so its HBM latency overlaps the passes and the upwind-trace work
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) cp_async8(A + swz<D, N>(R + a * SP + b * SQ), p.du + g0 + a * SP + b * SQ);
       cp_async_commit();
     }
+    // volume terms of P and Q and this cell's downwind traces along P and Q
+    double trP[N], trQ[N];
+    const unsigned char oP = ci.out[P], oQ = QA ? ci.out[Q] : (unsigned char)kOutNone;
+    if (oP != kOutNone) {
+      if (sgP == 0) pass_P<N, 0, FIRST, true>(acc, uv, s0P, slP, trP);
+      else pass_P<N, 1, FIRST, true>(acc, uv, s0P, slP, trP);
+    } else {
+      if (sgP == 0) pass_P<N, 0, FIRST, false>(acc, uv, s0P, slP, trP);
+      else pass_P<N, 1, FIRST, false>(acc, uv, s0P, slP, trP);
+    }
+    if constexpr (QA) {
+      if (oQ != kOutNone) {
+        if (sgQ == 0) pass_Q<N, 0, true>(acc, uv, s0Q, slQ, trQ);
+        else pass_Q<N, 1, true>(acc, uv, s0Q, slQ, trQ);
+      } else {
+        if (sgQ == 0) pass_Q<N, 0, false>(acc, uv, s0Q, slQ, trQ);
+        else pass_Q<N, 1, false>(acc, uv, s0Q, slQ, trQ);
+      }
+    }
+    // publish the downwind traces (dim 0 only ever feeds the carry; it is always P of phase 0)
+    if (oP == kOutCarry) store_vec<N>(carry_out + N * r, trP, false);
+    else if (oP == kOutPub) store_vec<N>(p.tbuf[P] + ((size_t)ci.unit * p.UC + ci.cu) * G::FN + (size_t)N * r, trP, true);
+    if constexpr (QA) {
+      if (oQ == kOutPub)
+        store_vec<N>(p.tbuf[Q] + ((size_t)ci.unit * p.UC + ci.cu) * G::FN + (size_t)N * r, trQ, true);
+    }
   }
-  // publish: one release per warp and phase (only phases somebody waits for)
-  if ((p.pubmask >> PH) & 1) {
-    __syncwarp();
-    if (warp_leader) red_release_add(p.flags + (size_t)b * NPH1 + PH);
-  }
-  if (!active) return;
 
-  // 3./4. upwind traces and rank-1 lifts
-  if (!haveP) upwind_trace<D, N, PH, SP, SQ>(p, ci, P, sgP, R, r, C, tP);
+  // upwind traces and rank-1 lifts
+  {
+    double t[N];
+    upwind_trace<D, N, SP, SQ>(p, ci, P, R, r, Ug, carry_in, t);
+    if (sgP == 0) {
 #pragma unroll
-  for (int bb = 0; bb < N; ++bb) tP[bb] *= fma(slP, T.xi[bb], s0P);
-  if (sgP == 0) lift_P<N, 0>(acc, tP);
-  else lift_P<N, 1>(acc, tP);
+      for (int b = 0; b < N; ++b) {
+        const double tb = t[b] * fma(slP, T.xi[b], s0P);
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[0][a], tb, acc[a][b]);
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        const double tb = t[b] * fma(slP, T.xi[b], s0P);
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[1][a], tb, acc[a][b]);
+      }
+    }
+  }
   if constexpr (QA) {
-    if (!haveQ) upwind_trace<D, N, PH, SQ, SP>(p, ci, Q, sgQ, R, r, C, tQ);
+    double t[N];
+    upwind_trace<D, N, SQ, SP>(p, ci, Q, R, r, Ug, carry_in, t);
+    if (sgQ == 0) {
 #pragma unroll
-    for (int a = 0; a < N; ++a) tQ[a] *= fma(slQ, T.xi[a], s0Q);
-    if (sgQ == 0) lift_Q<N, 0>(acc, tQ);
-    else lift_Q<N, 1>(acc, tQ);
+      for (int a = 0; a < N; ++a) {
+        const double ta = t[a] * fma(slQ, T.xi[a], s0Q);
+#pragma unroll
+        for (int b = 0; b < N; ++b) acc[a][b] = fma(T.lam[0][b], ta, acc[a][b]);
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const double ta = t[a] * fma(slQ, T.xi[a], s0Q);
+#pragma unroll
+        for (int b = 0; b < N; ++b) acc[a][b] = fma(T.lam[1][b], ta, acc[a][b]);
+      }
+    }
   }
 
   if constexpr (!LAST) {
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int bb = 0; bb < N; ++bb) ACC[paddr<EB16>(a * SP + bb * SQ, eb, peb)] = acc[a][bb];
+      for (int b = 0; b < N; ++b) A[swz<D, N>(R + a * SP + b * SQ)] = acc[a][b];
   } else if constexpr (MODE == kModeAdvection) {
     // weak form: v = M (M^-1 A u), M_qq = |J| prod_i w_{q_i}
     const double wr = tp.wr;
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int bb = 0; bb < N; ++bb) __stcs(p.out + g0 + a * SP + bb * SQ, acc[a][bb] * (wr * (T.w[a] * T.w[bb])));
+      for (int b = 0; b < N; ++b) __stcs(p.out + g0 + a * SP + b * SQ, acc[a][b] * (wr * (T.w[a] * T.w[b])));
   } else {
     // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU
-    if constexpr (MODE == kModeRK && !HD_DU_DIRECT) cp_async_wait<0>();
+    if constexpr (MODE == kModeRK) cp_async_wait<0>();
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int bb = 0; bb < N; ++bb) {
-        const int o = paddr<EB16>(a * SP + bb * SQ, eb, peb);
-        double dun = acc[a][bb];
-        if constexpr (MODE == kModeRK)
-          dun = fma(p.rk_a, HD_DU_DIRECT ? __ldcs(p.du + g0 + a * SP + bb * SQ) : ACC[o], dun);
-        __stcs(p.du + g0 + a * SP + bb * SQ, dun);
-        __stcs(p.out + g0 + a * SP + bb * SQ, fma(p.rk_b, dun, U[o]));
+      for (int b = 0; b < N; ++b) {
+        const int o = swz<D, N>(R + a * SP + b * SQ);
+        double dun = acc[a][b];
+        if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
+        __stcs(p.du + g0 + a * SP + b * SQ, dun);
+        __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, dun, U[o]));
       }
   }
 }
 
-// One item (all phases). Not inlined into the persistent loop, so that item-invariant values are
-// not hoisted out of it and kept live in registers across the whole loop.
+// One group (all phases). Not inlined into the persistent loop, so that group-invariant values are not
+// hoisted out of it and kept live in registers across the whole loop.
 template <int D, int N, int MODE>
-__device__ __noinline__ void process_item(const CellParams &p, const CellInfo &ci, const double *stab, int b,
-                                          int k, int r, int C, const double *U, double *ACC, bool warp_leader,
-                                          bool active) {
+__device__ __noinline__ void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
+                                           const double *Ug, double *ACC, const double *carry_in, double *carry_out,
+                                           bool active) {
   using G = CGeo<D, N>;
-  run_phase<D, N, MODE, 0>(p, ci, stab, b, k, r, C, U, ACC, warp_leader, active);
+  run_phase<D, N, MODE, 0>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
   if constexpr (G::NPH > 1) {
     __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, b, k, r, C, U, ACC, warp_leader, active);
+    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
   }
   if constexpr (G::NPH > 2) {
     __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, b, k, r, C, U, ACC, warp_leader, active);
+    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
   }
 }
 
+template <int D, int N>
+__host__ __device__ constexpr int cell_smem_bytes(int CT) {
+  using G = CGeo<D, N>;
+  return (3 * CT * G::ND + 2 * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo);
+}
+
+// Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
 template <int D, int N, int MODE>
-__global__ void __launch_bounds__(256, 2) cell_kernel(const __grid_constant__ CellParams p, int C) {
+__global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constant__ CellParams p) {
   using G = CGeo<D, N>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int bufp = padded(((C * G::ND + 15) / 16) * 16);
+  const int CT = p.CT;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  double *ACC = smem + 2 * bufp;
-  double *stab = ACC + bufp;                                        // xi[8], w[8]
-  CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);         // C entries
+  double *Ubuf[2] = {smem, smem + CT * G::ND};
+  double *ACC = smem + 2 * CT * G::ND;
+  double *carry[2] = {ACC + CT * G::ND, ACC + CT * G::ND + G::FN};
+  double *stab = carry[1] + G::FN;                           // xi[8], w[8]
+  CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);  // CT entries
   const int tid = threadIdx.x;
   const int k = tid / G::NT;
   const int r = tid - k * G::NT;
-  const bool active = k < C;
-  const int lane = tid & 31;
-  const bool warp_leader = lane == 0 && (tid - lane) < C * G::NT;
+  const bool active = k < CT;
   if (tid < 8) {
     stab[tid] = tid < N ? c_tab[N].xi[tid] : 0.0;
     stab[8 + tid] = tid < N ? c_tab[N].w[tid] : 0.0;
   }
+  if ((int)blockIdx.x >= p.nunits) return;
 
-  int b = blockIdx.x;
-  if (b >= p.nitems) return;
-  auto copy_item = [&](int first_cell, double *dst) {
+  auto copy_group = [&](int first_cell, double *dst) {
     const double *src = p.u + (size_t)first_cell * G::ND;
-    const int total = C * G::ND;
+    const int total = CT * G::ND;
     if constexpr (G::ND % 2 == 0) {
-      for (int i = tid; i < (total >> 1); i += blockDim.x) cp_async16(dst + padded(2 * i), src + 2 * i);
+      for (int i = tid; i < (total >> 1); i += blockDim.x) {
+        const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
+        cp_async16(dst + kc * G::ND + swz<D, N>(x), src + e);
+      }
     } else {
-      for (int i = tid; i < total; i += blockDim.x) cp_async8(dst + padded(i), src + i);
+      for (int i = tid; i < total; i += blockDim.x) cp_async8(dst + i, src + i);
     }
   };
-  copy_item(item_first_cell<D>(p, b, C), smem);
+
+  int u = blockIdx.x, gi = 0, it = 0;
+  copy_group(group_first_cell<D>(p, u, 0), Ubuf[0]);
   cp_async_commit();
-  for (int it = 0; b < p.nitems; b += gridDim.x, ++it) {
-    const int bn = b + gridDim.x;
-    __syncthreads();  // previous item finished: info and the other U buffer are free
-    if (bn < p.nitems) copy_item(item_first_cell<D>(p, bn, C), smem + ((it + 1) & 1) * bufp);
+  int prev_unit = -1;
+  while (u < p.nunits) {
+    // next group (this unit or the first group of the next unit)
+    int un = u, gn = gi + 1;
+    if (gn >= p.GPU) {
+      un = u + gridDim.x;
+      gn = 0;
+    }
+    __syncthreads();  // previous group finished: info, carry and the other U buffer are free
+    if (prev_unit >= 0 && tid == 0) {
+      // the previous unit's traces are all written (barrier above): publish it
+      __threadfence();
+      *(volatile int *)(p.flags + prev_unit) = p.epoch;
+    }
+    prev_unit = -1;
+    if (un < p.nunits) copy_group(group_first_cell<D>(p, un, gn), Ubuf[(it + 1) & 1]);
     cp_async_commit();
-    decode_coords<D>(p, b, C, info);
-    __syncthreads();
-    decode_links<D>(p, b, C, info);
+    if (tid < CT) decode_cell<D>(p, u, gi, tid, info[tid]);
     cp_async_wait<1>();
     __syncthreads();
-    const double *U = smem + (it & 1) * bufp;
-    process_item<D, N, MODE>(p, info[active ? k : 0], stab, b, k, r, C, U, ACC, warp_leader, active);
-    // item done: publish phase NPH (ring slots of the last phase use it as "finished reading")
-    if ((p.pubmask >> G::NPH) & 1) {
-      __syncwarp();
-      if (warp_leader) red_release_add(p.flags + (size_t)b * (G::NPH + 1) + G::NPH);
-    }
+    // every thread enters (the phases are separated by CTA barriers); padding threads idle inside
+    process_group<D, N, MODE>(p, info[active ? k : 0], stab, k, r, Ubuf[it & 1], ACC, carry[(gi + 1) & 1],
+                              carry[gi & 1], active);
+    if (gn == 0 && p.pubany) prev_unit = u;
+    u = un;
+    gi = gn;
+    ++it;
   }
   cp_async_wait<0>();
+  if (prev_unit >= 0) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      *(volatile int *)(p.flags + prev_unit) = p.epoch;
+    }
+  }
 }
 
 }  // namespace hd

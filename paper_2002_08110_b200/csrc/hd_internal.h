@@ -32,40 +32,72 @@ void build_tables(int n, Tables1D &t);
 
 enum Mode : int { kModeAdvection = 0, kModeRK = 1, kModeRKFirst = 2 };
 
-// Trace mode of a dimension:
-//   kTraceNone: every consumer reads its upwind neighbour cell and forms the trace itself
-//   kTraceRing: producers publish downwind traces into an L2-resident ring of items
-//   kTraceFar : producers publish into a full-size buffer (consumer is many items later)
-enum TraceMode : int { kTraceNone = 0, kTraceRing = 1, kTraceFar = 2 };
+// x-space partition of the ranks (hd_plan.cpp)
+struct Partition {
+  int d = 0, d_x = 0, P = 1, rank = 0;
+  int xparts[3] = {1, 1, 1};  // ranks per x dim
+  int bcoord[3] = {0, 0, 0};  // this rank's block coordinates
+  long long off[6] = {0, 0, 0, 0, 0, 0}, len[6] = {1, 1, 1, 1, 1, 1};  // local box of the global cell grid
+  long long ncells_local = 0;
+};
+// halo of one x dim (hd_plan.cpp): what crosses the rank faces along it
+struct HaloDim {
+  bool active = false;
+  int left = 0, right = 0;             // neighbour ranks along the dim
+  std::vector<int> send_left;          // local cells (low face, a_i < 0) whose traces go to the left rank
+  std::vector<int> send_right;         // local cells (high face, a_i > 0) whose traces go to the right rank
+  long long n_from_left = 0, n_from_right = 0;  // traces received (positions with a_i > 0 / a_i < 0)
+  std::vector<int> slot;               // per face-plane position: slot in the receive buffer
+};
+int host_cell_sign(const hd_mesh_desc &ds, const double *h, int d, int i, const long long *cg);
+bool make_partition(const hd_mesh_desc &ds, Partition &pt, std::string &err);
+void make_halo(const hd_mesh_desc &ds, const Partition &pt, const double *h, int i, HaloDim &hd);
 
-// Kernel parameters (passed by value as __grid_constant__).
+// Kernel parameters of the fused cell kernel (passed by value as __grid_constant__).
+// Work decomposition: a group = CT cells consecutive along dim 0; a unit = the groups one
+// CTA processes back to back: a pencil of L_0 cells (pencil mode, CT | L_0) or a single group holding
+// whole pencils (L_0 | CT).
 struct CellParams {
   const double *u;        // operator input (never written by the kernel)
   double *out;            // A-mode: v; RK-mode: U_new
   double *du;             // RK-mode: dU (read unless first stage, written)
-  int ncells;             // owned cells (< 2^31)
-  int nitems;             // work items = ncells / C (C consecutive cells along dim 0)
   int mode;
-  int target;             // flag value that marks "published in this launch" (epoch * warps per item)
+  int epoch;              // unit-flag value that marks "complete in this launch"
   double rk_a, rk_b;      // stage coefficients A_s, B_s
   double dtfac;           // 1 (A-mode) or dt (RK-mode): folded into the line speeds
   double jdet;            // |J| = prod h_i
-  // geometry (local box of cells)
-  int L[kMaxD];           // cells per dim
-  int IL[kMaxD];          // item-grid extents (IL[0] = L[0] / C)
-  int istride[kMaxD];     // item-index stride per dim (traversal order)
+  int nunits;             // units of this launch
+  int CT;                 // cells per group
+  int GPU;                // groups per unit
+  int UC;                 // cells per unit (trace-buffer slot size)
+  int pencil;             // 1: pencil mode
+  int pubany;             // some dim publishes traces (unit flags needed)
+  int L[kMaxD];           // cells per dim (local box)
   int lstride[kMaxD];     // cell-index stride per dim (memory order)
+  int ustride[kMaxD];     // unit-index stride per dim (pencil mode, dims >= 1)
   double lo[kMaxD], h[kMaxD], inv_h[kMaxD];
   double a_const[kMaxD];
   double a_lin[kMaxD][kMaxD];
-  // upwind traces
-  int tmode[kMaxD];       // TraceMode per dim
-  int dirneg[kMaxD];      // traversal direction of trace dims: 1 if a_i < 0 everywhere
-  int rmask[kMaxD];       // ring slots - 1 (kTraceRing)
-  double *tbuf[kMaxD];    // trace storage per dim: [slot][cell in item][n^(d-1)]
-  int *flags;             // [nitems][phases + 1] publication counters
-  int pubmask;            // bit ph: phase ph's counter is waited on (publish it)
-  int debug;
+  int pub[kMaxD];         // 1: dim publishes traces into tbuf (far buffer, one slot per unit)
+  int dirneg[kMaxD];      // published dims: traversal reversed (a_i < 0 on the whole box)
+  double *tbuf[kMaxD];    // trace storage per dim: [unit][cell in unit][n^(d-1)]
+  int *flags;             // [nunits] unit completion flags (value = epoch)
+  // multi-rank: the local box starts at global cell coordinates coff; along a split x dim
+  // a neighbour outside the box is on another rank and its trace comes from the halo buffer
+  int coff[kMaxD];
+  int xsplit[kMaxD];
+  const double *hbuf[kMaxD];  // received traces per x dim: [slot][n^(d-1)]
+  const int *hslot[kMaxD];    // face-plane position -> slot
+};
+
+// Halo pack (hd_kernels.cu): traces of the listed cells (entry e: cell index, dim, sign) into
+// out[e][n^(d-1)], face points in the consumer's phase layout.
+struct PackParams {
+  const double *u;
+  double *out;
+  const int *cells;     // [nent]
+  const int *dimsg;     // [nent]: dim | (sign << 8)
+  long long nent;
 };
 
 // Stream kernels
@@ -79,7 +111,7 @@ struct StreamParams {
 struct FillParams {
   double *u;
   long long ncells;
-  long long nx_local, cx_begin;
+  long long off[kMaxD], len[kMaxD];  // local box in the global cell grid
   long long L[kMaxD];
   double lo[kMaxD], h[kMaxD];
   int d_x, d;
@@ -92,24 +124,30 @@ cudaError_t upload_tables(int n, const Tables1D &t);
 cudaError_t launch_cell_kernel(int d, int n, const CellParams &p, cudaStream_t s, long long *launches, int grid);
 cudaError_t launch_mass_kernel(int d, int n, const StreamParams &p, cudaStream_t s, long long *launches, int sms);
 cudaError_t launch_fill_kernel(int d, int n, const FillParams &p, cudaStream_t s, long long *launches);
+cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s, long long *launches);
 bool cell_kernel_supported(int d, int n);
-// Kernel geometry for (d, n, L0): cells per item C (a divisor of L0), threads per CTA, phases,
-// warps per item, and the persistent grid size (co-resident CTAs).
+// Kernel geometry for (d, n) on a local box with L0 cells along dim 0 and ncells cells: cells per group
+// CT, pencil mode, threads per CTA, dynamic smem bytes, phases.
 struct CellGeometry {
-  int C, threads, phases, warps_per_item, smem;
+  int CT, pencil, GPU, threads, smem, phases;
 };
-CellGeometry cell_geometry(int d, int n, int L0);
-cudaError_t cell_grid_size(int d, int n, int L0, int mode, int sms, int *grid);
+CellGeometry cell_geometry(int d, int n, int L0, long long ncells);
+cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd
+
+namespace hd {
+struct NcclApi;  // dlopen'ed NCCL entry points (hd_api.cpp)
+}
 
 struct hd_mesh {
   hd_mesh_desc desc;
   int d, n;
   long long nd;            // n^d
   long long ncells_global, ncells_local;
-  long long cx_total, cx_begin, cx_end, nx_local, nv;
+  long long cx_total, cx_begin, cx_end;  // flat x-cell range of the local box (-1: not contiguous)
   long long owned_dofs;
+  hd::Partition pt;        // local box and rank grid
   double h[6];
   double jdet;
   hd::Tables1D tab;
@@ -117,9 +155,20 @@ struct hd_mesh {
   long long launches;
   // trace machinery (device buffers owned by the mesh)
   hd::CellGeometry geo;
-  int tmode[6], rmask[6], dirneg[6];
+  int nunits;
+  int pub[6], dirneg[6];
   double *tbuf[6];
   int *flags;
   long long epoch;
   int grid;
+  // halo (nranks > 1): per x dim receive buffer and slot table; one send buffer for all dims, laid
+  // out per dim as [to the right rank][to the left rank]
+  hd::HaloDim halo[3];
+  double *hbuf[3];
+  int *hslot[3];
+  long long send_off_right[3], send_off_left[3];  // entry offsets into the send buffer
+  long long nsend;                                // entries
+  int *pack_cells, *pack_dimsg;
+  double *sendbuf;
+  void *nccl_comm;         // ncclComm_t when the NCCL transport is used
 };

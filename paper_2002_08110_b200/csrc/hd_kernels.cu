@@ -118,25 +118,22 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillP
   const long long total = p.ncells * ND;
   for (long long gl = blockIdx.x * (long long)blockDim.x + threadIdx.x; gl < total;
        gl += (long long)gridDim.x * blockDim.x) {
-    const long long cell = gl / ND;
-    int m = (int)(gl % ND);
-    long long lcx = cell % p.nx_local, cv = cell / p.nx_local;
-    long long cx = p.cx_begin + lcx;
+    long long cell = gl / ND;
+    const int m0 = (int)(gl % ND);
+    int m = m0;
     double z[D];
+    long long gcell = 0, gs = 1;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      long long c;
-      if (i < p.d_x) { c = cx % p.L[i]; cx /= p.L[i]; }
-      else { c = cv % p.L[i]; cv /= p.L[i]; }
+      const long long c = p.off[i] + cell % p.len[i];  // global cell coordinate
+      cell /= p.len[i];
       z[i] = p.lo[i] + ((double)c + T.xi[m % N]) * p.h[i];
       m /= N;
+      gcell += c * gs;
+      gs *= p.L[i];
     }
     // global DoF index (reading C19) for the counter-based generator
-    long long cxg = p.cx_begin + lcx;
-    long long cxtot = 1;
-    for (int i = 0; i < p.d_x; ++i) cxtot *= p.L[i];
-    const long long gcell = (cell / p.nx_local) * cxtot + cxg;
-    const long long gg = gcell * ND + (gl % ND);
+    const long long gg = gcell * ND + m0;
     const unsigned long long bits = splitmix64((unsigned long long)gg + (p.seed << 40));
     const double U = (double)(bits >> 11) * (1.0 / 9007199254740992.0);
     double val;
@@ -161,6 +158,54 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillP
 }
 
 // ---------------------------------------------------------------------------------------------
+// Halo pack: the downwind trace of each listed cell along its listed dim, written in the
+// consumer's phase layout (face point f = N r + l: rest digits r, partner tile digit l), with the same
+// summation order as the cell kernel, so a trace that crosses ranks has the bits it would have had
+// inside one rank.
+template <int D, int N>
+__device__ __forceinline__ int face_offset(int X, int f) {
+  using G = CGeo<D, N>;
+  const int ph = (X == 0 || X == D - 1) ? 0 : (X + 1) / 2;
+  const int P = G::P(ph), Q = G::Q(ph);
+  const int partner = X == P ? Q : P;
+  int r = f / N;
+  const int l = f - r * N;
+  int R = 0, nj = 1;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (j != P && j != Q) {
+      R += (r % N) * nj;
+      r /= N;
+    }
+    nj *= N;
+  }
+  int sp = 1;
+  for (int j = 0; j < partner; ++j) sp *= N;
+  return R + l * sp;
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
+  using G = CGeo<D, N>;
+  const long long total = p.nent * G::FN;
+  for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < total;
+       gi += (long long)gridDim.x * blockDim.x) {
+    const long long e = gi / G::FN;
+    const int f = (int)(gi - e * G::FN);
+    const int ds = p.dimsg[e];
+    const int X = ds & 255, S = ds >> 8;
+    int sx = 1;
+    for (int j = 0; j < X; ++j) sx *= N;
+    const double *src = p.u + (size_t)p.cells[e] * G::ND + face_offset<D, N>(X, f);
+    const double *tau = c_tab[N].tau[S];
+    double s = tau[0] * __ldg(src);
+#pragma unroll
+    for (int j = 1; j < N; ++j) s = fma(tau[j], __ldg(src + j * sx), s);
+    p.out[gi] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Host-side dispatch over the instantiated (d, n) set.
 cudaError_t upload_tables(int n, const Tables1D &t) {
   return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables1D), sizeof(Tables1D) * n, cudaMemcpyHostToDevice);
@@ -169,27 +214,36 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 namespace {
 
 template <int D, int N>
-CellGeometry geometry_dn(int L0) {
+CellGeometry geometry_dn(int L0, long long ncells) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
-  int C = 1;
-  for (int c = 1; c <= L0 && c * G::NT <= 256; ++c) {
-    const int bufp = padded(((c * G::ND + 15) / 16) * 16);
-    const int smem = 3 * bufp * 8 + 128 +c * (int)sizeof(CellInfo) + 16;
-    if (L0 % c == 0 && smem <= 110 * 1024) C = c;
+  const int maxCT = 256 / G::NT;
+  constexpr int kSmemMax = 113 * 1024;
+  if (L0 <= maxCT) {
+    // multi-pencil groups: m whole pencils per group
+    const long long npen = ncells / L0;
+    int m = 1;
+    for (int c = 1; c * L0 <= maxCT; ++c)
+      if (npen % c == 0 && cell_smem_bytes<D, N>(c * L0) <= kSmemMax) m = c;
+    g.CT = m * L0;
+    g.pencil = 0;
+    g.GPU = 1;
+  } else {
+    int CT = 1;
+    for (int c = 1; c <= maxCT; ++c)
+      if (L0 % c == 0 && cell_smem_bytes<D, N>(c) <= kSmemMax) CT = c;
+    g.CT = CT;
+    g.pencil = 1;
+    g.GPU = L0 / CT;
   }
-  g.C = C;
-  g.threads = ((C * G::NT + 31) / 32) * 32;
-  g.warps_per_item = (C * G::NT + 31) / 32;
-  const int bufp = padded(((C * G::ND + 15) / 16) * 16);
-  g.smem = 3 * bufp * 8 + 128 +C * (int)sizeof(CellInfo) + 16;
+  g.threads = ((g.CT * G::NT + 31) / 32) * 32;
+  g.smem = cell_smem_bytes<D, N>(g.CT);
   return g;
 }
 
 template <int D, int N, int MODE>
-cudaError_t grid_impl(int L0, int sms, int *grid) {
-  const CellGeometry g = geometry_dn<D, N>(L0);
+cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
   auto kern = cell_kernel<D, N, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
   if (e != cudaSuccess) return e;
@@ -202,14 +256,11 @@ cudaError_t grid_impl(int L0, int sms, int *grid) {
 
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
-  const CellGeometry g = geometry_dn<D, N>(p.L[0]);
-  int grid = grid_max < p.nitems ? grid_max : p.nitems;
+  const CellGeometry g = geometry_dn<D, N>(p.L[0], (long long)p.nunits * p.UC);
+  int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
-  int C = g.C;
-  void *args[] = {const_cast<CellParams *>(&p), &C};
-  // cooperative launch: every CTA is co-resident, which the producer/consumer flags rely on
-  return cudaLaunchCooperativeKernel((const void *)cell_kernel<D, N, MODE>, dim3(grid), dim3(g.threads), args,
-                                     (size_t)g.smem, s);
+  cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 template <int D, int N>
@@ -226,18 +277,17 @@ cudaError_t launch_cell_dn(const CellParams &p, cudaStream_t s, int grid_max) {
 }
 
 template <int D, int N>
-cudaError_t grid_dn(int L0, int mode, int sms, int *grid) {
+cudaError_t grid_dn(const CellGeometry &g, int sms, int *grid) {
   if constexpr (!CGeo<D, N>::OK) {
     return cudaErrorNotSupported;
   } else {
     // all modes share the geometry; take the minimum co-residency over them
     int g0 = 0, g1 = 0, g2 = 0;
-    cudaError_t e = grid_impl<D, N, kModeAdvection>(L0, sms, &g0);
-    if (e == cudaSuccess) e = grid_impl<D, N, kModeRK>(L0, sms, &g1);
-    if (e == cudaSuccess) e = grid_impl<D, N, kModeRKFirst>(L0, sms, &g2);
-    (void)mode;
-    int g = g0 < g1 ? g0 : g1;
-    *grid = g < g2 ? g : g2;
+    cudaError_t e = grid_impl<D, N, kModeAdvection>(g, sms, &g0);
+    if (e == cudaSuccess) e = grid_impl<D, N, kModeRK>(g, sms, &g1);
+    if (e == cudaSuccess) e = grid_impl<D, N, kModeRKFirst>(g, sms, &g2);
+    int m = g0 < g1 ? g0 : g1;
+    *grid = m < g2 ? m : g2;
     return e;
   }
 }
@@ -269,6 +319,16 @@ cudaError_t launch_fill_dn(const FillParams &p, cudaStream_t s) {
   if (grid > 148LL * 64) grid = 148LL * 64;
   if (grid < 1) grid = 1;
   fill_kernel<D, N><<<(unsigned)grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int D, int N>
+cudaError_t launch_pack_dn(const PackParams &p, cudaStream_t s) {
+  long long total = p.nent * (long long)ipow(N, D - 1);
+  long long grid = (total + 255) / 256;
+  if (grid > 148LL * 16) grid = 148LL * 16;
+  if (grid < 1) return cudaSuccess;
+  pack_kernel<D, N><<<(unsigned)grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -310,10 +370,16 @@ cudaError_t launch_fill_kernel(int d, int n, const FillParams &p, cudaStream_t s
   if (launches) ++*launches;
   HD_DISPATCH(launch_fill_dn, cudaErrorNotSupported, p, s)
 }
+cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s, long long *launches) {
+  if (launches) ++*launches;
+  HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
+}
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0) { HD_DISPATCH(geometry_dn, CellGeometry{}, L0) }
-cudaError_t cell_grid_size(int d, int n, int L0, int mode, int sms, int *grid) {
-  HD_DISPATCH(grid_dn, cudaErrorNotSupported, L0, mode, sms, grid)
+CellGeometry cell_geometry(int d, int n, int L0, long long ncells) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, ncells)
+}
+cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
+  HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)
 }
 
 }  // namespace hd

@@ -1,0 +1,172 @@
+"""Multi-rank host logic on the CPU: the x-space partition and the halo
+plan of include/hd.h (hd_partition_info, hd_halo_list), which need no GPU.
+
+* every cell is owned by exactly one rank and v-cells are never split (v part undivided);
+* the traces rank r sends to rank q are exactly, and in the same order, those q expects from r -- checked
+  across real processes: world_size-2 ``gloo`` groups exchange their plans with all_gather_object;
+* the union of the receive lists is exactly the set of (cell, dim) pairs whose UPWIND neighbour (sign
+  of a_i at the cell centre, C3/C11) is owned by another rank -- recomputed here independently with numpy.
+"""
+import itertools
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2002_08110_b200 import configs, halo_list, partition_info
+
+
+def _spec(d_x, d_v, k, cells, lo, hi, a_const, a_lin=None):
+    d = d_x + d_v
+    if a_lin is None:
+        a_lin = [[0.0] * d for _ in range(d)]
+    return dict(d_x=d_x, d_v=d_v, k=k, cells=list(cells), lo=list(lo), hi=list(hi), a_const=list(a_const),
+                a_lin=[list(r) for r in a_lin], flux="upwind")
+
+
+def _vlasov(d_x, d_v, cells, k=1):
+    d = d_x + d_v
+    lin = [[0.0] * d for _ in range(d)]
+    for i in range(min(d_x, d_v)):
+        lin[i][d_x + i] = 1.0
+    ac = [0.0] * d_x + [0.3, -0.2, 0.1][:d_v]
+    lo = [0.0] * d_x + [-2.0] * d_v
+    hi = [1.0] * d_x + [2.0] * d_v
+    return _spec(d_x, d_v, k, cells, lo, hi, ac, lin)
+
+
+CASES = [
+    ("3d-const-P2", _spec(2, 1, 2, [4, 6, 3], [0] * 3, [1] * 3, [1.0, -0.7, 0.3]), 2, None),
+    ("4d-vlasov-P2", _vlasov(2, 2, [4, 6, 2, 4]), 2, None),
+    ("4d-vlasov-P4", _vlasov(2, 2, [4, 6, 2, 4]), 4, None),
+    ("5d-vlasov-P8", _vlasov(3, 2, [4, 4, 6, 2, 2]), 8, None),
+    ("5d-vlasov-P4-x0split", _vlasov(3, 2, [4, 4, 6, 2, 2]), 4, [4, 1, 1]),
+    ("6d-vlasov-P8", _vlasov(3, 3, [2, 2, 2, 2, 2, 2]), 8, None),
+]
+
+
+def _sign(spec, i, c):
+    """1 if a_i < 0 at the centre of the cell with global coordinates c (reading C11)."""
+    d = spec["d_x"] + spec["d_v"]
+    h = [(spec["hi"][j] - spec["lo"][j]) / spec["cells"][j] for j in range(d)]
+    a = spec["a_const"][i] + sum(spec["a_lin"][i][j] * (spec["lo"][j] + (c[j] + 0.5) * h[j]) for j in range(d))
+    return 1 if a < 0 else 0
+
+
+def _owner_map(spec, P, xparts):
+    d = spec["d_x"] + spec["d_v"]
+    owner = -np.ones(spec["cells"][::-1], dtype=np.int64).transpose()  # index [c0, c1, ...]
+    for r in range(P):
+        _, off, ln = partition_info(spec, r, P, xparts)
+        sl = tuple(slice(off[i], off[i] + ln[i]) for i in range(d))
+        assert np.all(owner[sl] == -1), "cells owned twice"
+        owner[sl] = r
+    assert np.all(owner >= 0), "cells owned by nobody"
+    return owner
+
+
+def _gid(spec, c):
+    g, s = 0, 1
+    for i, ci in enumerate(c):
+        g += ci * s
+        s *= spec["cells"][i]
+    return g
+
+
+@pytest.mark.parametrize("name,spec,P,xparts", CASES, ids=[c[0] for c in CASES])
+def test_partition_covers_and_halo_is_the_remote_upwind_set(name, spec, P, xparts):
+    d, d_x = spec["d_x"] + spec["d_v"], spec["d_x"]
+    owner = _owner_map(spec, P, xparts)
+    xp, off, ln = partition_info(spec, 0, P, xparts)
+    assert int(np.prod(xp)) == P
+    for i in range(d_x, d):
+        assert ln[i] == spec["cells"][i], "v dims must not be split"
+    # independent: (cell, dim) pairs whose upwind neighbour is remote, per receiving rank
+    expect = {r: set() for r in range(P)}
+    for c in itertools.product(*[range(n) for n in spec["cells"]]):
+        for i in range(d_x):
+            up = 1 if _sign(spec, i, c) else -1
+            cn = list(c)
+            cn[i] = (c[i] + up) % spec["cells"][i]
+            if owner[tuple(cn)] != owner[c]:
+                expect[owner[c]].add((_gid(spec, c), i, owner[tuple(cn)]))
+    for r in range(P):
+        got = set()
+        for i in range(d_x):
+            for which in (2, 3):
+                peer, ids = halo_list(spec, r, P, i, which, xparts)
+                assert len(ids) == len(set(ids))
+                got |= {(g, i, peer) for g in ids}
+        assert got == expect[r], f"rank {r}: halo receive set differs from the remote-upwind set"
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, cases, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        errors = []
+        for name, spec, P, xparts in cases:
+            # this process plays ranks rank, rank + world, ... of the P-rank partition
+            mine = {}
+            for r in range(rank, P, world):
+                for i in range(spec["d_x"]):
+                    for which in range(4):
+                        mine[(r, i, which)] = halo_list(spec, r, P, i, which, xparts)
+            allp = [None] * world
+            dist.all_gather_object(allp, mine)
+            plan = {}
+            for part in allp:
+                plan.update(part)
+            for r in range(rank, P, world):
+                for i in range(spec["d_x"]):
+                    # what r receives from its left (which 2) is what the left rank sends right (which 1)
+                    for recv_w, send_w in ((2, 1), (3, 0)):
+                        peer, rids = plan[(r, i, recv_w)]
+                        if peer < 0:
+                            continue
+                        back, sids = plan[(peer, i, send_w)]
+                        if back != r or sids != rids:
+                            errors.append(f"{name}: rank {r} dim {i} which {recv_w} vs rank {peer}")
+        q.put((rank, errors))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_plans_match_across_gloo_ranks():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, CASES, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, errors in res:
+        assert not errors, errors
+
+
+def test_config_partitions():
+    """The bench configs shard as documented: 6D/5D over 2/4/8 ranks (x-slab when it divides)."""
+    for name in ("5d", "6d"):
+        spec = configs.CONFIGS[name]["spec"]
+        for P in (2, 4, 8):
+            xp, off, ln = partition_info(spec, P - 1, P)
+            assert int(np.prod(xp)) == P
+            assert all(spec["cells"][i] % xp[i] == 0 for i in range(3))
+        # 2 ranks split the slowest x dim (x-slab)
+        assert partition_info(spec, 0, 2)[0] == [1, 1, 2]
