@@ -113,6 +113,7 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.CT = g.CT;
   p.GPU = g.GPU;
   p.pencil = g.pencil;
+  p.ws = g.ws;
   p.UC = g.pencil ? (int)m->pt.len[0] : g.CT;
   p.nunits = m->nunits;
   p.jdet = m->jdet;
@@ -138,10 +139,18 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
     for (int j = 0; j < d; ++j) p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
     p.pub[i] = m->pub[i];
     p.dirneg[i] = m->pub[i] ? m->dirneg[i] : 0;
+    // a dim follows its speed when a_i depends on slower dims only (then its sign is constant along
+    // the traversal of dim i and of all faster dims)
+    bool follow = g.pencil && i >= 1 && m->pt.len[i] > 1;
+    for (int j = 0; j < i; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
+    if (const char *e = getenv("HD_FOLLOW")) follow = follow && atoi(e) != 0;
+    p.follow[i] = follow ? 1 : 0;
     p.tbuf[i] = m->tbuf[i];
     p.pubany |= m->pub[i];
   }
   p.flags = m->flags;
+  p.skew = g.pencil && g.GPU > 1 ? 1 : 0;
+  if (const char *e = getenv("HD_SKEW")) p.skew = p.skew && atoi(e) != 0;
   // one epoch per cell-kernel launch: unit flags hold the epoch of their last completion
   m->epoch += 1;
   p.epoch = (int)m->epoch;
@@ -458,7 +467,13 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     delete m;
     return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
   }
-  m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local);
+  {
+    // kernel variant: warp-specialised (default) or the single-role kernel (HD_KERNEL=base)
+    int ws = 1;
+    if (const char *kv = getenv("HD_KERNEL")) ws = std::strcmp(kv, "base") != 0;
+    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local, ws);
+    if (ws && m->geo.smem > 227 * 1024) m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local, 0);
+  }
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / pt.len[0] : m->ncells_local / m->geo.CT);
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
   if (e != cudaSuccess) {

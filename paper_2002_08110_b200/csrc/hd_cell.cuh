@@ -19,6 +19,9 @@
 //     group) says it is complete; otherwise -- and for all other dims -- the thread reads the
 //     neighbour cell's lines itself (L2) and contracts them. Nobody ever waits for another CTA.
 #pragma once
+#ifndef HD_WS_LB
+#define HD_WS_LB 384
+#endif
 #ifndef HD_MINB
 #define HD_MINB 2
 #endif
@@ -42,15 +45,23 @@ struct CGeo {
   static constexpr bool OK = NT <= 256 && (3 * ND + 2 * FN + 16) * 8 + 256 <= 227 * 1024;
 };
 
-// Shared-memory element order of a cell: XOR swizzle that keeps (2e, 2e+1) pairs together and makes
-// every phase's tile access bank-conflict free for n = 4 (checked by tools: all phases of d = 4..6).
+// Shared-memory element order of a cell (n = 4, d >= 4): phys(x) = x + 4 (x >> 6) + 2 ((x >> 4) & 3), i.e.
+// padding after every 64 doubles plus a skew by digit 2. It keeps (2e, 2e+1) pairs together (16-byte
+// cp.async / LDS.128), makes every phase's tile access bank-conflict free (d = 4..6, checked by a
+// script over all phases), and is ADDITIVE over disjoint digit fields: phys(R + T) = phys(R) + phys(T)
+// -- so a thread's tile elements sit at phys(R) + compile-time offsets (immediate addressing).
 template <int D, int N>
-__host__ __device__ __forceinline__ constexpr int swz(int x) {
+__host__ __device__ __forceinline__ constexpr int phys(int x) {
   if constexpr (N == 4 && D >= 4) {
-    return x ^ (((x >> 6) & 3) << 2) ^ (((x >> 4) & 1) << 1);
+    return x + 4 * (x >> 6) + 2 * ((x >> 4) & 3);
   } else {
     return x;
   }
+}
+// smem stride of one cell (even: cells stay 16-byte aligned)
+template <int D, int N>
+__host__ __device__ constexpr int cell_stride() {
+  return ((phys<D, N>(ipow(N, D) - 1) + 1) + 1) / 2 * 2;
 }
 
 struct CellInfo {
@@ -93,32 +104,67 @@ __device__ __forceinline__ void cell_speed(const CellParams &p, int i, const int
   sg = (ab + half) < 0.0 ? 1 : 0;
 }
 
-// Pencil-mode unit decode: coordinates c_1..c_{D-1} (traversal coordinates t), pencil base cell and
-// the direction of dim 0 (1: a_0 < 0, groups processed from the far end).
+// Pencil-mode unit decode, slowest dim first: traversal coordinates t_j = (u / ustride_j) % L_j; a dim
+// that "follows" its speed (the sign of a_j depends only on slower dims, so it is constant along the
+// sweep) is traversed upwind -> downwind: c_j = L_j - 1 - t_j where a_j < 0. Then every upwind neighbour
+// along such a dim is an EARLIER unit. Returns the pencil's base cell, the dim-0 direction (1: a_0 < 0,
+// groups from the far end) and the skew: the pencil starts at group (-sum_j t_j) mod GPU, so a unit's
+// upwind neighbours along every dim (same round) are exactly one group ahead of it.
 template <int D>
-__device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c)[kMaxD], int (&t)[kMaxD], int &dir0) {
-  int base = 0;
-  c[0] = 0;
-  t[0] = 0;
+__device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c)[kMaxD], int (&t)[kMaxD], int &dir0,
+                                             int &skew) {
+  int base = 0, tsum = 0;
 #pragma unroll
-  for (int j = 1; j < D; ++j) {
+  for (int j = 0; j < kMaxD; ++j) {
+    c[j] = 0;
+    t[j] = 0;
+  }
+#pragma unroll
+  for (int j = D - 1; j >= 1; --j) {
     const int tj = (u / p.ustride[j]) % p.L[j];
     t[j] = tj;
-    c[j] = p.dirneg[j] ? p.L[j] - 1 - tj : tj;
+    tsum += tj;
+    int neg = p.dirneg[j];
+    if (p.follow[j]) {
+      double b;
+      cell_speed<D>(p, j, c, b, neg);  // faster coordinates are still 0: a_j does not depend on them
+    }
+    c[j] = neg ? p.L[j] - 1 - tj : tj;
     base += c[j] * p.lstride[j];
   }
   double b0;
   cell_speed<D>(p, 0, c, b0, dir0);
+  skew = p.skew ? (p.GPU - tsum % p.GPU) % p.GPU : 0;
   return base;
+}
+
+// Unit index (pencil mode) of the pencil holding a cell with coordinates c.
+template <int D>
+__device__ __forceinline__ int unit_of(const CellParams &p, const int (&c)[kMaxD]) {
+  int cc[kMaxD], u = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxD; ++j) cc[j] = 0;
+#pragma unroll
+  for (int j = D - 1; j >= 1; --j) {
+    int neg = p.dirneg[j];
+    if (p.follow[j]) {
+      double b;
+      cell_speed<D>(p, j, cc, b, neg);
+    }
+    cc[j] = c[j];
+    u += (neg ? p.L[j] - 1 - c[j] : c[j]) * p.ustride[j];
+  }
+  return u;
 }
 
 // First cell (memory order) of group gi of unit u.
 template <int D>
 __device__ __forceinline__ int group_first_cell(const CellParams &p, int u, int gi) {
   if (!p.pencil) return u * p.CT;
-  int c[kMaxD], t[kMaxD], dir0;
-  const int base = pencil_decode<D>(p, u, c, t, dir0);
-  const int g = dir0 ? p.GPU - 1 - gi : gi;
+  int c[kMaxD], t[kMaxD], dir0, skew;
+  const int base = pencil_decode<D>(p, u, c, t, dir0, skew);
+  int g = (gi + skew) % p.GPU;
+  if (dir0) g = p.GPU - 1 - g;
   return base + g * p.CT;
 }
 
@@ -128,9 +174,10 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, 
   int c[kMaxD], t[kMaxD];
   int first;
   if (p.pencil) {
-    int dir0;
-    const int base = pencil_decode<D>(p, u, c, t, dir0);
-    const int g = dir0 ? p.GPU - 1 - gi : gi;
+    int dir0, skew;
+    const int base = pencil_decode<D>(p, u, c, t, dir0, skew);
+    int g = (gi + skew) % p.GPU;
+    if (dir0) g = p.GPU - 1 - g;
     c[0] = g * p.CT + k;
     first = base + g * p.CT;
     ci.cu = c[0];
@@ -196,7 +243,11 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, 
         nb = nbcell - first;
       } else if (p.pub[i]) {
         if (t[i] > 0) {
-          const int pu = u - p.ustride[i];
+          int cn2[kMaxD];
+#pragma unroll
+          for (int j = 0; j < kMaxD; ++j) cn2[j] = c[j];
+          cn2[i] = cn;
+          const int pu = unit_of<D>(p, cn2);
           if (ld_acquire(p.flags + pu) >= p.epoch) {
             src = kSrcPub;
             slot = pu;
@@ -210,6 +261,30 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, 
     ci.nb[i] = nb;
     ci.slot[i] = slot;
   }
+}
+
+// Cell-local offset (dim-X digit 0) of face point f = N r + l of dim X in the phase layout of X: rest
+// digits r (dims other than the phase pair, ascending), partner tile digit l.
+template <int D, int N>
+__device__ __forceinline__ int face_offset(int X, int f) {
+  using G = CGeo<D, N>;
+  const int ph = (X == 0 || X == D - 1) ? 0 : (X + 1) / 2;
+  const int P = G::P(ph), Q = G::Q(ph);
+  const int partner = X == P ? Q : P;
+  int r = f / N;
+  const int l = f - r * N;
+  int R = 0, nj = 1;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (j != P && j != Q) {
+      R += (r % N) * nj;
+      r /= N;
+    }
+    nj *= N;
+  }
+  int sp = 1;
+  for (int j = 0; j < partner; ++j) sp *= N;
+  return R + l * sp;
 }
 
 // Per-thread phase constants for rest index r. sx, sw: the 1D nodes and weights staged in smem.
@@ -308,13 +383,14 @@ __device__ __forceinline__ void trace_global(const double *nb, int S, double (&t
   }
 }
 template <int D, int N, int SX, int SY>
-__device__ __forceinline__ void trace_smem(const double *cellbuf, int R, int S, double (&t)[N]) {
+__device__ __forceinline__ void trace_smem(const double *cellbuf, int pR, int S, double (&t)[N]) {
   const double *tau = c_tab[N].tau[S];
+  const double *c = cellbuf + pR;
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    double s = tau[0] * cellbuf[swz<D, N>(R + l * SY)];
+    double s = tau[0] * c[phys<D, N>(l * SY)];
 #pragma unroll
-    for (int j = 1; j < N; ++j) s = fma(tau[j], cellbuf[swz<D, N>(R + j * SX + l * SY)], s);
+    for (int j = 1; j < N; ++j) s = fma(tau[j], c[phys<D, N>(j * SX + l * SY)], s);
     t[l] = s;
   }
 }
@@ -353,14 +429,23 @@ __device__ __forceinline__ void load_vec(const double *src, double (&t)[N], bool
 
 // Obtain the upwind trace of dim X for this thread (X is the tile's first index when FIRST_IDX, i.e.
 // X = P: lines along P, face points indexed by b; else X = Q).
-template <int D, int N, int SX, int SY>
-__device__ __forceinline__ void upwind_trace(const CellParams &p, const CellInfo &ci, int X, int R, int r,
-                                             const double *Ugroup, const double *carry_in, double (&t)[N]) {
+template <int D, int N, int SX, int SY, bool WS>
+__device__ __forceinline__ void upwind_trace(const CellParams &p, const CellInfo &ci, int X, int R, int pR, int r,
+                                             const double *Ugroup, const double *carry_in, const double *TRk,
+                                             double (&t)[N]) {
   using G = CGeo<D, N>;
   const int S = ci.sg[X];
+  if constexpr (WS) {
+    // warp-specialised kernel: the loader warps staged every non-local trace in smem
+    const int src = ci.src[X];
+    if (src != kSrcGroup && src != kSrcCarry) {
+      load_vec<N>(TRk + X * G::FN + N * r, t, false);
+      return;
+    }
+  }
   switch (ci.src[X]) {
     case kSrcGroup:
-      trace_smem<D, N, SX, SY>(Ugroup + (size_t)ci.nb[X] * G::ND, R, S, t);
+      trace_smem<D, N, SX, SY>(Ugroup + (size_t)ci.nb[X] * cell_stride<D, N>(), pR, S, t);
       break;
     case kSrcCarry:
       load_vec<N>(carry_in + N * r, t, false);
@@ -377,10 +462,10 @@ __device__ __forceinline__ void upwind_trace(const CellParams &p, const CellInfo
   }
 }
 
-template <int D, int N, int MODE, int PH>
+template <int D, int N, int MODE, int PH, bool WS>
 __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
                                           const double *Ug, double *ACC, const double *carry_in, double *carry_out,
-                                          bool active) {
+                                          const double *TRk, bool active) {
   if (!active) return;  // padding threads of the CTA: only the barriers between phases
   using G = CGeo<D, N>;
   constexpr int P = G::P(PH), Q = G::Q(PH);
@@ -392,8 +477,10 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   ThreadPhase tp;
   thread_phase<D, N, PH, LAST && MODE == kModeAdvection>(p, r, stab, stab + 8, tp);
   const int R = tp.R;
-  const double *U = Ug + (size_t)k * G::ND;
-  double *A = ACC + (size_t)k * G::ND;
+  const int pR = phys<D, N>(R);
+  constexpr int CS = cell_stride<D, N>();
+  const double *U = Ug + (size_t)k * CS + pR;
+  double *A = ACC + (size_t)k * CS + pR;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
   const size_t g0 = (size_t)ci.cell * G::ND + R;
   // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line (a_i varies only with the other dims)
@@ -409,7 +496,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       for (int b = 0; b < N; ++b)
 #pragma unroll
         for (int a = 0; a < N; a += 2) {
-          const double2 v = *reinterpret_cast<const double2 *>(U + swz<D, N>(R + a + b * SQ));
+          const double2 v = *reinterpret_cast<const double2 *>(U + phys<D, N>(a + b * SQ));
           uv[a][b] = v.x;
           uv[a + 1][b] = v.y;
         }
@@ -417,21 +504,22 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) uv[a][b] = U[swz<D, N>(R + a * SP + b * SQ)];
+        for (int b = 0; b < N; ++b) uv[a][b] = U[phys<D, N>(a * SP + b * SQ)];
     }
     if constexpr (!FIRST) {
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) acc[a][b] = A[swz<D, N>(R + a * SP + b * SQ)];
+        for (int b = 0; b < N; ++b) acc[a][b] = A[phys<D, N>(a * SP + b * SQ)];
     }
     if constexpr (LAST && MODE == kModeRK) {
+      const unsigned long long pol = evict_first_policy();
       // dU of the tile -> this thread's own ACC positions (already consumed), asynchronously; read back
       // in the epilogue, so its HBM latency overlaps the passes and the upwind-trace work
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) cp_async8(A + swz<D, N>(R + a * SP + b * SQ), p.du + g0 + a * SP + b * SQ);
+        for (int b = 0; b < N; ++b) cp_async8_ef(A + phys<D, N>(a * SP + b * SQ), p.du + g0 + a * SP + b * SQ, pol);
       cp_async_commit();
     }
     // volume terms of P and Q and this cell's downwind traces along P and Q
@@ -465,7 +553,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   // upwind traces and rank-1 lifts
   {
     double t[N];
-    upwind_trace<D, N, SP, SQ>(p, ci, P, R, r, Ug, carry_in, t);
+    upwind_trace<D, N, SP, SQ, WS>(p, ci, P, R, pR, r, Ug, carry_in, TRk, t);
     if (sgP == 0) {
 #pragma unroll
       for (int b = 0; b < N; ++b) {
@@ -484,7 +572,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   }
   if constexpr (QA) {
     double t[N];
-    upwind_trace<D, N, SQ, SP>(p, ci, Q, R, r, Ug, carry_in, t);
+    upwind_trace<D, N, SQ, SP, WS>(p, ci, Q, R, pR, r, Ug, carry_in, TRk, t);
     if (sgQ == 0) {
 #pragma unroll
       for (int a = 0; a < N; ++a) {
@@ -506,7 +594,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int b = 0; b < N; ++b) A[swz<D, N>(R + a * SP + b * SQ)] = acc[a][b];
+      for (int b = 0; b < N; ++b) A[phys<D, N>(a * SP + b * SQ)] = acc[a][b];
   } else if constexpr (MODE == kModeAdvection) {
     // weak form: v = M (M^-1 A u), M_qq = |J| prod_i w_{q_i}
     const double wr = tp.wr;
@@ -521,7 +609,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) {
-        const int o = swz<D, N>(R + a * SP + b * SQ);
+        const int o = phys<D, N>(a * SP + b * SQ);
         double dun = acc[a][b];
         if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
         __stcs(p.du + g0 + a * SP + b * SQ, dun);
@@ -530,28 +618,42 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   }
 }
 
+// named barrier among the first `count` threads (warp multiples)
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
 // One group (all phases). Not inlined into the persistent loop, so that group-invariant values are not
-// hoisted out of it and kept live in registers across the whole loop.
-template <int D, int N, int MODE>
-__device__ __noinline__ void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
+// hoisted out of it and kept live in registers across the whole loop. WS: only the compute warps run it
+// (phase barrier = named barrier 5 over `ncompute` threads).
+#ifndef HD_PG_INLINE
+#define HD_PG_INLINE __noinline__
+#endif
+template <int D, int N, int MODE, bool WS>
+__device__ HD_PG_INLINE void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
                                            const double *Ug, double *ACC, const double *carry_in, double *carry_out,
-                                           bool active) {
+                                           const double *TRk, bool active, int ncompute) {
   using G = CGeo<D, N>;
-  run_phase<D, N, MODE, 0>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
+  run_phase<D, N, MODE, 0, WS>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, TRk, active);
   if constexpr (G::NPH > 1) {
-    __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
+    if constexpr (WS) bar_sync(5, ncompute);
+    else __syncthreads();
+    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0), WS>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, TRk, active);
   }
   if constexpr (G::NPH > 2) {
-    __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
+    if constexpr (WS) bar_sync(5, ncompute);
+    else __syncthreads();
+    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0), WS>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, TRk, active);
   }
 }
 
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * G::ND + 2 * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo);
+  return (3 * CT * cell_stride<D, N>() + 2 * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo);
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
@@ -561,9 +663,10 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  double *Ubuf[2] = {smem, smem + CT * G::ND};
-  double *ACC = smem + 2 * CT * G::ND;
-  double *carry[2] = {ACC + CT * G::ND, ACC + CT * G::ND + G::FN};
+  constexpr int CS = cell_stride<D, N>();
+  double *Ubuf[2] = {smem, smem + CT * CS};
+  double *ACC = smem + 2 * CT * CS;
+  double *carry[2] = {ACC + CT * CS, ACC + CT * CS + G::FN};
   double *stab = carry[1] + G::FN;                           // xi[8], w[8]
   CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);  // CT entries
   const int tid = threadIdx.x;
@@ -582,10 +685,13 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     if constexpr (G::ND % 2 == 0) {
       for (int i = tid; i < (total >> 1); i += blockDim.x) {
         const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
-        cp_async16(dst + kc * G::ND + swz<D, N>(x), src + e);
+        cp_async16(dst + kc * CS + phys<D, N>(x), src + e);
       }
     } else {
-      for (int i = tid; i < total; i += blockDim.x) cp_async8(dst + i, src + i);
+      for (int i = tid; i < total; i += blockDim.x) {
+        const int kc = i / G::ND, x = i - kc * G::ND;
+        cp_async8(dst + kc * CS + phys<D, N>(x), src + i);
+      }
     }
   };
 
@@ -613,8 +719,8 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     cp_async_wait<1>();
     __syncthreads();
     // every thread enters (the phases are separated by CTA barriers); padding threads idle inside
-    process_group<D, N, MODE>(p, info[active ? k : 0], stab, k, r, Ubuf[it & 1], ACC, carry[(gi + 1) & 1],
-                              carry[gi & 1], active);
+    process_group<D, N, MODE, false>(p, info[active ? k : 0], stab, k, r, Ubuf[it & 1], ACC, carry[(gi + 1) & 1],
+                                     carry[gi & 1], nullptr, active, 0);
     if (gn == 0 && p.pubany) prev_unit = u;
     u = un;
     gi = gn;
@@ -628,6 +734,164 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       *(volatile int *)(p.flags + prev_unit) = p.epoch;
     }
   }
+}
+
+}  // namespace hd
+
+namespace hd {
+
+// ---------------------------------------------------------------------------------------------------
+// Warp-specialised variant (1 CTA per SM): NCW compute warps run the phases from shared memory only;
+// 4 loader warps run up to two groups ahead -- decode, cp.async of the group's cells, cp.async of the
+// published / halo traces, and the neighbour-read traces (coalesced L2 loads + contraction) into a
+// double-buffered trace buffer TR[stage][cell][dim][n^(d-1)]. Hand-off by named barriers:
+//   1 + s: FULL[s]  (loader arrives, compute syncs)     3 + s: EMPTY[s] (compute arrives, loader syncs)
+//   5: compute-internal phase barrier                    6: loader-internal barrier
+constexpr int kLoaderThreads = 128;
+
+template <int D, int N>
+__host__ __device__ constexpr int ws_smem_bytes(int CT) {
+  using G = CGeo<D, N>;
+  return (3 * CT * cell_stride<D, N>() + 2 * CT * D * G::FN + 2 * G::FN + 16) * 8 + 2 * CT * (int)sizeof(CellInfo);
+}
+
+template <int D, int N>
+__device__ __forceinline__ void ws_unit_group(const CellParams &p, int j, int &u, int &gi) {
+  // j-th group of this CTA's sequence
+  const int ju = j / p.GPU;
+  gi = j - ju * p.GPU;
+  u = blockIdx.x + ju * gridDim.x;
+}
+
+template <int D, int N, int MODE>
+__global__ void __launch_bounds__(HD_WS_LB, 1) cell_kernel_ws(const __grid_constant__ CellParams p) {
+  using G = CGeo<D, N>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int CT = p.CT;
+  const int NC = ((CT * G::NT + 31) / 32) * 32;  // compute threads
+  double *smem = reinterpret_cast<double *>(smem_raw);
+  constexpr int CS = cell_stride<D, N>();
+  double *Ubuf0 = smem;
+  double *ACC = smem + 2 * CT * CS;
+  double *TR0 = ACC + CT * CS;                          // [2][CT][D][FN]
+  double *carry0 = TR0 + 2 * CT * D * G::FN;            // [2][FN]
+  double *stab = carry0 + 2 * G::FN;                    // xi[8], w[8]
+  CellInfo *info0 = reinterpret_cast<CellInfo *>(stab + 16);  // [2][CT]
+  const int tid = threadIdx.x;
+  if (tid < 8) {
+    stab[tid] = tid < N ? c_tab[N].xi[tid] : 0.0;
+    stab[8 + tid] = tid < N ? c_tab[N].w[tid] : 0.0;
+  }
+  if ((int)blockIdx.x >= p.nunits) return;
+  __syncthreads();
+  const int my_units = (p.nunits - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int ngroups = my_units * p.GPU;
+  const int NTOT = NC + kLoaderThreads;
+
+  if (tid >= NC) {
+    // ------------------------------ loader warps ------------------------------
+    const int lt = tid - NC;
+    for (int j = 0; j < ngroups; ++j) {
+      const int s = j & 1;
+      int u, gi;
+      ws_unit_group<D, N>(p, j, u, gi);
+      if (j >= 2) bar_sync(3 + s, NTOT);  // compute finished group j-2: stage s is free
+      CellInfo *info = info0 + s * CT;
+      for (int k = lt; k < CT; k += kLoaderThreads) decode_cell<D>(p, u, gi, k, info[k]);
+      const int first = group_first_cell<D>(p, u, gi);
+      // the group's cells
+      {
+        double *dst = Ubuf0 + s * CT * CS;
+        const double *src = p.u + (size_t)first * G::ND;
+        const int total = CT * G::ND;
+        if constexpr (G::ND % 2 == 0) {
+          for (int i = lt; i < (total >> 1); i += kLoaderThreads) {
+            const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
+            cp_async16(dst + kc * CS + phys<D, N>(x), src + e);
+          }
+        } else {
+          for (int i = lt; i < total; i += kLoaderThreads) {
+            const int kc = i / G::ND, x = i - kc * G::ND;
+            cp_async8(dst + kc * CS + phys<D, N>(x), src + i);
+          }
+        }
+      }
+      bar_sync(6, kLoaderThreads);  // info visible to all loader threads
+      double *TR = TR0 + s * CT * D * G::FN;
+      // published / halo traces: plain copies (already in the phase layout)
+      for (int k = 0; k < CT; ++k) {
+        const CellInfo &ci = info[k];
+#pragma unroll
+        for (int X = 0; X < D; ++X) {
+          const int src = ci.src[X];
+          if (src != kSrcPub && src != kSrcHalo) continue;
+          const double *g = src == kSrcPub ? p.tbuf[X] + ((size_t)ci.slot[X] * p.UC + ci.cu) * G::FN
+                                           : p.hbuf[X] + (size_t)ci.slot[X] * G::FN;
+          double *d = TR + (k * D + X) * G::FN;
+          if constexpr (G::FN % 2 == 0) {
+            for (int i = lt; i < G::FN / 2; i += kLoaderThreads) cp_async16(d + 2 * i, g + 2 * i);
+          } else {
+            for (int i = lt; i < G::FN; i += kLoaderThreads) cp_async8(d + i, g + i);
+          }
+        }
+      }
+      cp_async_commit();
+      // neighbour-read traces: face points distributed with the lowest rest digit fastest (coalesced)
+      for (int k = 0; k < CT; ++k) {
+        const CellInfo &ci = info[k];
+#pragma unroll
+        for (int X = 0; X < D; ++X) {
+          if (ci.src[X] != kSrcDirect) continue;
+          constexpr int NR = G::FN / N;
+          const double *tau = c_tab[N].tau[ci.sg[X]];
+          const double *nb = p.u + (size_t)ci.nb[X] * G::ND;
+          int sx = 1;
+          for (int q = 0; q < X; ++q) sx *= N;
+          double *d = TR + (k * D + X) * G::FN;
+          for (int f2 = lt; f2 < G::FN; f2 += kLoaderThreads) {
+            const int l = f2 / NR, rr = f2 - l * NR;
+            const int f = rr * N + l;
+            const double *src = nb + face_offset<D, N>(X, f);
+            double v[N];
+#pragma unroll
+            for (int q = 0; q < N; ++q) v[q] = __ldg(src + q * sx);
+            double acc = tau[0] * v[0];
+#pragma unroll
+            for (int q = 1; q < N; ++q) acc = fma(tau[q], v[q], acc);
+            d[f] = acc;
+          }
+        }
+      }
+      cp_async_wait<0>();
+      bar_arrive(1 + s, NTOT);  // stage s full
+    }
+    return;
+  }
+
+  // ------------------------------ compute warps ------------------------------
+  const int k = tid / G::NT;
+  const int r = tid - k * G::NT;
+  const bool active = k < CT;
+  for (int j = 0; j < ngroups; ++j) {
+    const int s = j & 1;
+    int u, gi;
+    ws_unit_group<D, N>(p, j, u, gi);
+    bar_sync(1 + s, NTOT);  // wait for stage s
+    const CellInfo *info = info0 + s * CT;
+    const double *Ug = Ubuf0 + s * CT * CS;
+    const double *TRk = TR0 + (s * CT + (active ? k : 0)) * D * G::FN;
+    process_group<D, N, MODE, true>(p, info[active ? k : 0], stab, k, r, Ug, ACC, carry0 + ((gi + 1) & 1) * G::FN,
+                                    carry0 + (gi & 1) * G::FN, TRk, active, NC);
+    // all compute threads are done with stage s, ACC and the carry of this group
+    bar_sync(5, NC);
+    if (j + 2 < ngroups) bar_arrive(3 + s, NTOT);
+    if (gi == p.GPU - 1 && p.pubany && tid == 0) {
+      // the unit's published traces are all written (barrier above): publish the unit
+      __threadfence();
+      *(volatile int *)(p.flags + u) = p.epoch;
+    }
+  }
+  cp_async_wait<0>();
 }
 
 }  // namespace hd

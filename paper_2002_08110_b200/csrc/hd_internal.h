@@ -72,6 +72,7 @@ struct CellParams {
   int UC;                 // cells per unit (trace-buffer slot size)
   int pencil;             // 1: pencil mode
   int pubany;             // some dim publishes traces (unit flags needed)
+  int ws;                 // 1: warp-specialised kernel (loader warps stage all non-local traces)
   int L[kMaxD];           // cells per dim (local box)
   int lstride[kMaxD];     // cell-index stride per dim (memory order)
   int ustride[kMaxD];     // unit-index stride per dim (pencil mode, dims >= 1)
@@ -80,6 +81,8 @@ struct CellParams {
   double a_lin[kMaxD][kMaxD];
   int pub[kMaxD];         // 1: dim publishes traces into tbuf (far buffer, one slot per unit)
   int dirneg[kMaxD];      // published dims: traversal reversed (a_i < 0 on the whole box)
+  int follow[kMaxD];      // pencil mode, dims >= 1: traversal follows the sign of a_i (depends on slower dims only)
+  int skew;               // pencil mode: skewed pencil start (see pencil_decode)
   double *tbuf[kMaxD];    // trace storage per dim: [unit][cell in unit][n^(d-1)]
   int *flags;             // [nunits] unit completion flags (value = epoch)
   // multi-rank: the local box starts at global cell coordinates coff; along a split x dim
@@ -129,9 +132,9 @@ bool cell_kernel_supported(int d, int n);
 // Kernel geometry for (d, n) on a local box with L0 cells along dim 0 and ncells cells: cells per group
 // CT, pencil mode, threads per CTA, dynamic smem bytes, phases.
 struct CellGeometry {
-  int CT, pencil, GPU, threads, smem, phases;
+  int CT, pencil, GPU, threads, smem, phases, ws;
 };
-CellGeometry cell_geometry(int d, int n, int L0, long long ncells);
+CellGeometry cell_geometry(int d, int n, int L0, long long ncells, int ws);
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd

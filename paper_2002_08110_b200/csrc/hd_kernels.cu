@@ -40,6 +40,16 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+// 8-byte cp.async with an L2 eviction-priority hint (streams read exactly once: dU)
+__device__ __forceinline__ void cp_async8_ef(void *smem_dst, const void *gsrc, unsigned long long pol) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory"); }
@@ -163,28 +173,6 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillP
 // summation order as the cell kernel, so a trace that crosses ranks has the bits it would have had
 // inside one rank.
 template <int D, int N>
-__device__ __forceinline__ int face_offset(int X, int f) {
-  using G = CGeo<D, N>;
-  const int ph = (X == 0 || X == D - 1) ? 0 : (X + 1) / 2;
-  const int P = G::P(ph), Q = G::Q(ph);
-  const int partner = X == P ? Q : P;
-  int r = f / N;
-  const int l = f - r * N;
-  int R = 0, nj = 1;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    if (j != P && j != Q) {
-      R += (r % N) * nj;
-      r /= N;
-    }
-    nj *= N;
-  }
-  int sp = 1;
-  for (int j = 0; j < partner; ++j) sp *= N;
-  return R + l * sp;
-}
-
-template <int D, int N>
 __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
   using G = CGeo<D, N>;
   const long long total = p.nent * G::FN;
@@ -214,37 +202,39 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 namespace {
 
 template <int D, int N>
-CellGeometry geometry_dn(int L0, long long ncells) {
+CellGeometry geometry_dn(int L0, long long ncells, int ws) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
+  g.ws = ws;
   const int maxCT = 256 / G::NT;
-  constexpr int kSmemMax = 113 * 1024;
+  const int kSmemMax = ws ? 227 * 1024 : 113 * 1024;
+  auto smem_of = [&](int c) { return ws ? ws_smem_bytes<D, N>(c) : cell_smem_bytes<D, N>(c); };
   if (L0 <= maxCT) {
     // multi-pencil groups: m whole pencils per group
     const long long npen = ncells / L0;
     int m = 1;
     for (int c = 1; c * L0 <= maxCT; ++c)
-      if (npen % c == 0 && cell_smem_bytes<D, N>(c * L0) <= kSmemMax) m = c;
+      if (npen % c == 0 && smem_of(c * L0) <= kSmemMax) m = c;
     g.CT = m * L0;
     g.pencil = 0;
     g.GPU = 1;
   } else {
     int CT = 1;
     for (int c = 1; c <= maxCT; ++c)
-      if (L0 % c == 0 && cell_smem_bytes<D, N>(c) <= kSmemMax) CT = c;
+      if (L0 % c == 0 && smem_of(c) <= kSmemMax) CT = c;
     g.CT = CT;
     g.pencil = 1;
     g.GPU = L0 / CT;
   }
-  g.threads = ((g.CT * G::NT + 31) / 32) * 32;
-  g.smem = cell_smem_bytes<D, N>(g.CT);
+  g.threads = ((g.CT * G::NT + 31) / 32) * 32 + (ws ? kLoaderThreads : 0);
+  g.smem = smem_of(g.CT);
   return g;
 }
 
 template <int D, int N, int MODE>
 cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
-  auto kern = cell_kernel<D, N, MODE>;
+  auto kern = g.ws ? cell_kernel_ws<D, N, MODE> : cell_kernel<D, N, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
   if (e != cudaSuccess) return e;
   int occ = 0;
@@ -256,10 +246,11 @@ cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
 
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
-  const CellGeometry g = geometry_dn<D, N>(p.L[0], (long long)p.nunits * p.UC);
+  const CellGeometry g = geometry_dn<D, N>(p.L[0], (long long)p.nunits * p.UC, p.ws);
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
-  cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  if (p.ws) cell_kernel_ws<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  else cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -375,8 +366,8 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s
   HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0, long long ncells) {
-  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, ncells)
+CellGeometry cell_geometry(int d, int n, int L0, long long ncells, int ws) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, ncells, ws)
 }
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
   HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)

@@ -1,0 +1,23 @@
+#!/bin/bash
+# tests + env-variant quick benches + ncu of the 6D RK kernel (summarised on the box)
+O=gpurun_out
+export PATH=/usr/local/cuda/bin:$PATH
+if [ -z "$SKIP_TESTS" ]; then
+timeout 1200 python -m pytest tests -m gpu -q -x ${PYTEST_ARGS} > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+tail -15 $O/pytest_gpu.log
+fi
+: > $O/quick.txt
+CONFIGS="${CONFIGS:-5d 6d}" STEPS=3 bash tools/quick_bench.sh ws >> $O/quick.txt 2>&1
+CONFIGS="${CONFIGS:-5d 6d}" STEPS=3 bash tools/quick_bench.sh base HD_KERNEL=base >> $O/quick.txt 2>&1
+CONFIGS="${CONFIGS:-5d 6d}" STEPS=3 bash tools/quick_bench.sh ws-noskew HD_SKEW=0 >> $O/quick.txt 2>&1
+cat $O/quick.txt
+for c in ${NCU_CONFIGS:-6d}; do
+  tag=ws_$c
+  timeout 300 python tools/prof_driver.py --config $c --op rk --reps 2 > $O/plain_$tag.log 2>&1 && \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:cell_kernel -s 6 -c 1 \
+     -o $O/ncu_$tag python tools/prof_driver.py --config $c --op rk --reps 2 > $O/ncu_$tag.log 2>&1
+  python tools/ncu_summary.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_$tag.txt 2>&1
+  sz=$(stat -c %s $O/ncu_$tag.ncu-rep 2>/dev/null || echo 0)
+  if [ "$sz" -gt 25000000 ]; then rm -f $O/ncu_$tag.ncu-rep; fi
+done
+du -sh $O
