@@ -106,6 +106,8 @@ hd_status ensure_tables(hd_mesh *m) {
   return HD_OK;
 }
 
+hd_status next_epoch(hd_mesh *m, hd::CellParams &p, cudaStream_t s);
+
 void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   std::memset(&p, 0, sizeof(p));
   const int d = m->d;
@@ -113,7 +115,6 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.CT = g.CT;
   p.GPU = g.GPU;
   p.pencil = g.pencil;
-  p.ws = g.ws;
   p.UC = g.pencil ? (int)m->pt.len[0] : g.CT;
   p.nunits = m->nunits;
   p.jdet = m->jdet;
@@ -138,65 +139,44 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
     p.a_const[i] = m->desc.a_const[i];
     for (int j = 0; j < d; ++j) p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
     p.pub[i] = m->pub[i];
-    p.dirneg[i] = m->pub[i] ? m->dirneg[i] : 0;
-    // a dim follows its speed when a_i depends on slower dims only (then its sign is constant along
-    // the traversal of dim i and of all faster dims)
-    bool follow = g.pencil && i >= 1 && m->pt.len[i] > 1;
-    for (int j = 0; j < i; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
-    if (const char *e = getenv("HD_FOLLOW")) follow = follow && atoi(e) != 0;
-    p.follow[i] = follow ? 1 : 0;
+    p.follow[i] = m->follow[i];
     p.tbuf[i] = m->tbuf[i];
     p.pubany |= m->pub[i];
   }
   p.flags = m->flags;
   p.skew = g.pencil && g.GPU > 1 ? 1 : 0;
   if (const char *e = getenv("HD_SKEW")) p.skew = p.skew && atoi(e) != 0;
-  // one epoch per cell-kernel launch: unit flags hold the epoch of their last completion
-  m->epoch += 1;
-  p.epoch = (int)m->epoch;
+  next_epoch(m, p, nullptr);
 }
 
-// Upwind-trace plan (DESIGN.md §6 "Upwind traces"). In pencil mode a dim i >= 1 publishes its traces
-// when (a) the sign of a_i is the same on the whole box (the traversal then follows it, so the producer
-// of a cell's upwind trace is exactly ustride_i units earlier) and (b) that producer is at least
-// HD_PUB_MIN (default 2) x grid units earlier, i.e. certainly finished in the steady state. All other
-// dims read their upwind neighbour cell themselves (it is then recent enough to be in L2).
+// Upwind-trace plan (DESIGN.md §6 "Upwind traces"). In pencil mode a dim i >= 1 FOLLOWS its speed when a_i
+// depends on slower dims only (its sign is then constant along the traversal of dim i and of all faster
+// dims, so the sweep can go upwind -> downwind); every following dim publishes its downwind traces for
+// the neighbour one group later. HD_TRACE=0 turns publishing off (all upwind traces by direct reads).
 hd_status plan_traces(hd_mesh *m) {
   const int d = m->d;
   const hd::CellGeometry &g = m->geo;
   const long long fn = m->nd / m->n;  // face points
-  bool use = true;
-  if (const char *e = getenv("HD_TRACE")) use = atoi(e) != 0;
-  double pub_min = 2.0;
-  if (const char *e = getenv("HD_PUB_MIN")) pub_min = atof(e);
-  long long ustride = 1;
+  bool use = g.pencil && g.GPU <= 1023;
+  if (const char *e = getenv("HD_TRACE")) use = use && atoi(e) != 0;
   bool any = false;
   for (int i = 0; i < d; ++i) {
     m->pub[i] = 0;
-    m->dirneg[i] = 0;
+    m->follow[i] = 0;
     m->tbuf[i] = nullptr;
-    if (i >= 1) {
-      const long long us = ustride;
-      ustride *= m->pt.len[i];
-      if (!use || !g.pencil || m->pt.len[i] < 2 || (i < 3 && m->pt.xparts[i] > 1)) continue;
-      double amin = m->desc.a_const[i], amax = m->desc.a_const[i];
-      for (int j = 0; j < d; ++j) {
-        const double aj = m->desc.a_lin[6 * i + j];
-        amin += fmin(aj * m->desc.lo[j], aj * m->desc.hi[j]);
-        amax += fmax(aj * m->desc.lo[j], aj * m->desc.hi[j]);
-      }
-      if (!(amin >= 0.0 || amax <= 0.0)) continue;
-      if ((double)us < pub_min * m->grid) continue;
-      m->pub[i] = 1;
-      m->dirneg[i] = amax <= 0.0 && amin < 0.0 ? 1 : 0;
-      const size_t bytes = (size_t)m->ncells_local * fn * sizeof(double);
-      cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
-      }
-      any = true;
+    if (i == 0 || !g.pencil || m->pt.len[i] < 2) continue;
+    bool follow = true;
+    for (int j = 0; j < i; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
+    m->follow[i] = follow ? 1 : 0;
+    if (!follow || !use) continue;
+    m->pub[i] = 1;
+    const size_t bytes = (size_t)m->ncells_local * fn * sizeof(double);
+    cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
     }
+    any = true;
   }
   m->flags = nullptr;
   if (any) {
@@ -209,6 +189,21 @@ hd_status plan_traces(hd_mesh *m) {
     }
   }
   m->epoch = 0;
+  return HD_OK;
+}
+
+// Every cell-kernel launch is a new epoch; unit flags hold (epoch << 10) | steps done. Before the epoch
+// field overflows, the flags are cleared on the stream and the count restarts.
+hd_status next_epoch(hd_mesh *m, hd::CellParams &p, cudaStream_t s) {
+  m->epoch += 1;
+  if (m->epoch >= (1LL << 20)) {
+    if (m->flags) {
+      cudaError_t e = cudaMemsetAsync(m->flags, 0, (size_t)m->nunits * sizeof(int), s);
+      if (e != cudaSuccess) return cuda_fail(e, "flag reset");
+    }
+    m->epoch = 1;
+  }
+  p.epoch = (int)(m->epoch << 10);
   return HD_OK;
 }
 
@@ -467,13 +462,7 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     delete m;
     return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
   }
-  {
-    // kernel variant: warp-specialised (default) or the single-role kernel (HD_KERNEL=base)
-    int ws = 1;
-    if (const char *kv = getenv("HD_KERNEL")) ws = std::strcmp(kv, "base") != 0;
-    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local, ws);
-    if (ws && m->geo.smem > 227 * 1024) m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local, 0);
-  }
+  m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local);
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / pt.len[0] : m->ncells_local / m->geo.CT);
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
   if (e != cudaSuccess) {
@@ -511,7 +500,7 @@ hd_status hd_destroy_mesh(hd_mesh *m) {
 hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots) {
   if (!m) return fail(HD_ERR_ARG, "null mesh");
   for (int i = 0; i < m->d; ++i) {
-    if (tmode) tmode[i] = m->pub[i] ? 2 : 0;
+    if (tmode) tmode[i] = m->pub[i] ? 1 : 0;
     if (ring_slots) ring_slots[i] = 0;
   }
   return HD_OK;
@@ -694,8 +683,8 @@ namespace {
 hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
                        double b, double dtfac, bool first_launch, cudaStream_t s, bool exchange) {
   if (!first_launch) {
-    m->epoch += 1;
-    p.epoch = (int)m->epoch;
+    hd_status st = next_epoch(m, p, s);
+    if (st != HD_OK) return st;
   }
   if (exchange && m->desc.nranks > 1) {
     hd_status st = halo_pack(m, U, s);

@@ -6,24 +6,22 @@
 // the UPWIND neighbour's trace. One CTA iteration processes a GROUP of CT cells that are consecutive
 // along dim 0; threads own, per phase, an n x n register tile of a cell over a pair of dims (P, Q).
 //
-// Work units and upwind traces (the part that decides performance):
+// Work units and upwind traces (the part that decides performance; DESIGN.md §6 "Upwind traces"):
 //   * pencil mode (CT | L_0): a unit is the pencil of L_0 cells along dim 0, processed group by group
-//     by ONE CTA in the direction of a_0 (constant on the pencil). The dim-0 upwind trace of the
-//     group's upwind-end cell is the previous group's downwind trace, carried in smem (no global
-//     traffic, no inter-CTA wait); only the first group (periodic wrap) reads its neighbour.
-//   * multi-pencil mode (L_0 | CT): a group holds whole pencils; dim-0 (and any other in-group)
-//     neighbours are read from smem.
-//   * dims whose upwind neighbour unit is >= 2 x grid units earlier ("published" dims; their speed has
-//     one sign on the whole box, so the traversal follows it) get the trace from a trace buffer the
-//     producer wrote (n^(d-1) values, 1/n of a cell) when the producer's unit flag (one acquire per
-//     group) says it is complete; otherwise -- and for all other dims -- the thread reads the
-//     neighbour cell's lines itself (L2) and contracts them. Nobody ever waits for another CTA.
+//     by ONE CTA upwind -> downwind (a_0 has one sign on the pencil). The dim-0 trace of the group's
+//     upwind-end cell is the previous group's downwind trace, carried in smem.
+//   * every other dim whose traversal follows the sign of its speed PUBLISHES its downwind traces
+//     (n^(d-1) values, 1/n of a cell) into a per-dim buffer and a per-unit progress flag. Units are
+//     swept in direction-following order with a skewed start (pencil_decode), so a unit's upwind
+//     neighbours in the same round run exactly one group ahead: when a group starts, the traces it needs
+//     were written one group earlier and are still in L2; the consumer reads them once and discards the
+//     lines (no DRAM write-back). A trace that is not published yet (first groups, round seams, wraps)
+//     is formed from the neighbour cell itself (direct read). Nobody ever waits for another CTA.
+//   * multi-pencil mode (L_0 | CT, small d): a group holds whole pencils; in-group neighbours come
+//     from smem, the rest by direct reads.
 #pragma once
-#ifndef HD_WS_LB
-#define HD_WS_LB 384
-#endif
 #ifndef HD_MINB
-#define HD_MINB 2
+#define HD_MINB 1
 #endif
 
 namespace hd {
@@ -41,27 +39,21 @@ struct CGeo {
   static constexpr __host__ __device__ int P(int ph) { return ph == 0 ? 0 : 2 * ph - 1; }
   static constexpr __host__ __device__ int Q(int ph) { return ph == 0 ? D - 1 : 2 * ph; }
   static constexpr __host__ __device__ bool QA(int ph) { return ph == 0 || 2 * ph != D - 1; }
-  // one cell must fit: U double buffer + ACC + carry double buffer in ~112 KB (2 CTAs per SM)
   static constexpr bool OK = NT <= 256 && (3 * ND + 2 * FN + 16) * 8 + 256 <= 227 * 1024;
 };
 
-// Shared-memory element order of a cell (n = 4, d >= 4): phys(x) = x + 4 (x >> 6) + 2 ((x >> 4) & 3), i.e.
-// padding after every 64 doubles plus a skew by digit 2. It keeps (2e, 2e+1) pairs together (16-byte
-// cp.async / LDS.128), makes every phase's tile access bank-conflict free (d = 4..6, checked by a
-// script over all phases), and is ADDITIVE over disjoint digit fields: phys(R + T) = phys(R) + phys(T)
-// -- so a thread's tile elements sit at phys(R) + compile-time offsets (immediate addressing).
+// Shared-memory element order of a cell (n = 4, d >= 4): XOR swizzle of bits 1..3 with bits 4, 6, 7.
+// A bijection that keeps (2e, 2e+1) pairs together (16-byte cp.async / LDS.128) and makes every phase's
+// tile access bank-conflict free (d = 4..6, checked over all phases). It is LINEAR over GF(2):
+// swz(R + T) = swz(R) ^ swz(T) for disjoint digit fields, so a thread's tile element sits at
+// swz(R) ^ (compile-time constant): one LOP3 per element, no per-element index arithmetic.
 template <int D, int N>
-__host__ __device__ __forceinline__ constexpr int phys(int x) {
+__host__ __device__ __forceinline__ constexpr int swz(int x) {
   if constexpr (N == 4 && D >= 4) {
-    return x + 4 * (x >> 6) + 2 * ((x >> 4) & 3);
+    return x ^ (((x >> 6) & 3) << 2) ^ (((x >> 4) & 1) << 1);
   } else {
     return x;
   }
-}
-// smem stride of one cell (even: cells stay 16-byte aligned)
-template <int D, int N>
-__host__ __device__ constexpr int cell_stride() {
-  return ((phys<D, N>(ipow(N, D) - 1) + 1) + 1) / 2 * 2;
 }
 
 struct CellInfo {
@@ -89,9 +81,12 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void discard_l2_line(const void *p) {
+  asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
+}
 
-// sign of a_i on a cell with coordinates c (evaluated at the cell centre; constant on the cell by
-// reading C11). Identical arithmetic wherever it is needed, so all decisions agree bitwise.
+// sign of a_i on a cell with coordinates c (local box; global = c + coff), evaluated at the cell centre
+// (constant on the cell by reading C11). The host plan (hd_plan.cpp) evaluates the same fma sequence.
 template <int D>
 __device__ __forceinline__ void cell_speed(const CellParams &p, int i, const int (&c)[kMaxD], double &base, int &sg) {
   double ab = p.a_const[i], half = 0.0;
@@ -124,7 +119,7 @@ __device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c
     const int tj = (u / p.ustride[j]) % p.L[j];
     t[j] = tj;
     tsum += tj;
-    int neg = p.dirneg[j];
+    int neg = 0;
     if (p.follow[j]) {
       double b;
       cell_speed<D>(p, j, c, b, neg);  // faster coordinates are still 0: a_j does not depend on them
@@ -146,7 +141,7 @@ __device__ __forceinline__ int unit_of(const CellParams &p, const int (&c)[kMaxD
   for (int j = 0; j < kMaxD; ++j) cc[j] = 0;
 #pragma unroll
   for (int j = D - 1; j >= 1; --j) {
-    int neg = p.dirneg[j];
+    int neg = 0;
     if (p.follow[j]) {
       double b;
       cell_speed<D>(p, j, cc, b, neg);
@@ -157,110 +152,123 @@ __device__ __forceinline__ int unit_of(const CellParams &p, const int (&c)[kMaxD
   return u;
 }
 
+// memory group of processing step gi of a unit with direction dir0 and skew
+__device__ __forceinline__ int step_group(const CellParams &p, int gi, int dir0, int skew) {
+  const int g = (gi + skew) % p.GPU;
+  return dir0 ? p.GPU - 1 - g : g;
+}
+// processing step of memory group g
+__device__ __forceinline__ int group_step(const CellParams &p, int g, int dir0, int skew) {
+  const int gg = dir0 ? p.GPU - 1 - g : g;
+  return (gg - skew + p.GPU) % p.GPU;
+}
+
 // First cell (memory order) of group gi of unit u.
 template <int D>
 __device__ __forceinline__ int group_first_cell(const CellParams &p, int u, int gi) {
   if (!p.pencil) return u * p.CT;
   int c[kMaxD], t[kMaxD], dir0, skew;
   const int base = pencil_decode<D>(p, u, c, t, dir0, skew);
-  int g = (gi + skew) % p.GPU;
-  if (dir0) g = p.GPU - 1 - g;
-  return base + g * p.CT;
+  return base + step_group(p, gi, dir0, skew) * p.CT;
 }
 
-// Decode cell k of group gi of unit u (one thread per cell).
+// Decode dim `i` of cell k of group gi of unit u (dim 0 also writes the cell-level fields).
 template <int D>
-__device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, int k, CellInfo &ci) {
+__device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, int k, CellInfo &ci, int i) {
   int c[kMaxD], t[kMaxD];
   int first;
   if (p.pencil) {
     int dir0, skew;
     const int base = pencil_decode<D>(p, u, c, t, dir0, skew);
-    int g = (gi + skew) % p.GPU;
-    if (dir0) g = p.GPU - 1 - g;
+    const int g = step_group(p, gi, dir0, skew);
     c[0] = g * p.CT + k;
     first = base + g * p.CT;
-    ci.cu = c[0];
   } else {
     first = u * p.CT;
     int rr = first + k;
 #pragma unroll
+    for (int j = 0; j < kMaxD; ++j) {
+      c[j] = 0;
+      t[j] = 0;
+    }
+#pragma unroll
     for (int j = 0; j < D; ++j) {
       c[j] = rr % p.L[j];
       rr /= p.L[j];
-      t[j] = 0;
     }
-    ci.cu = k;
   }
   int cell = 0;
 #pragma unroll
   for (int j = 0; j < D; ++j) cell += c[j] * p.lstride[j];
-  ci.cell = cell;
-  ci.unit = u;
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    double base;
-    int sg;
-    cell_speed<D>(p, i, c, base, sg);
-    ci.base[i] = base;
-    ci.sg[i] = (unsigned char)sg;
-    const int up = sg ? 1 : -1;
-    int cn = c[i] + up;
-    const bool outside = cn < 0 || cn >= p.L[i];
-    if (cn < 0) cn += p.L[i];
-    if (cn >= p.L[i]) cn -= p.L[i];
-    const int nbcell = cell + (cn - c[i]) * p.lstride[i];
-    unsigned char src = kSrcDirect, out = kOutNone;
-    int nb = nbcell, slot = 0;
-    if (outside && p.xsplit[i]) {
-      // the upwind neighbour lives on another rank: its trace arrived in the halo buffer
-      src = kSrcHalo;
-      const int ls = p.lstride[i];
-      slot = p.hslot[i][(cell % ls) + (cell / (ls * p.L[i])) * ls];
-      if (i == 0 && p.pencil) {
-        const int kd = k - up;
-        if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
-      }
-    } else if (i == 0) {
-      if (!p.pencil) {
-        src = kSrcGroup;
-        nb = k + (cn - c[0]);
-      } else {
-        const int kk = k + up;
-        if (kk >= 0 && kk < p.CT) {
-          src = kSrcGroup;
-          nb = kk;
-        } else if (gi > 0) {
-          src = kSrcCarry;
-        }
-        // downwind-end cell of a group that has a successor in this unit feeds the carry
-        const int kd = k - up;
-        if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
-      }
-    } else {
-      if (!p.pencil && nbcell >= first && nbcell < first + p.CT) {
-        src = kSrcGroup;
-        nb = nbcell - first;
-      } else if (p.pub[i]) {
-        if (t[i] > 0) {
-          int cn2[kMaxD];
-#pragma unroll
-          for (int j = 0; j < kMaxD; ++j) cn2[j] = c[j];
-          cn2[i] = cn;
-          const int pu = unit_of<D>(p, cn2);
-          if (ld_acquire(p.flags + pu) >= p.epoch) {
-            src = kSrcPub;
-            slot = pu;
-          }
-        }
-      }
-      if (p.pub[i] && t[i] < p.L[i] - 1) out = kOutPub;
-    }
-    ci.src[i] = src;
-    ci.out[i] = out;
-    ci.nb[i] = nb;
-    ci.slot[i] = slot;
+  if (i == 0) {
+    ci.cell = cell;
+    ci.unit = u;
+    ci.cu = p.pencil ? c[0] : k;
   }
+  double base;
+  int sg;
+  cell_speed<D>(p, i, c, base, sg);
+  ci.base[i] = base;
+  ci.sg[i] = (unsigned char)sg;
+  const int up = sg ? 1 : -1;
+  int cn = c[i] + up;
+  const bool outside = cn < 0 || cn >= p.L[i];
+  if (cn < 0) cn += p.L[i];
+  if (cn >= p.L[i]) cn -= p.L[i];
+  const int nbcell = cell + (cn - c[i]) * p.lstride[i];
+  unsigned char src = kSrcDirect, out = kOutNone;
+  int nb = nbcell, slot = 0;
+  if (i == 0 && p.pencil) {
+    // downwind-end cell of a group that has a successor in this unit feeds the carry
+    const int kd = k - up;
+    if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
+  }
+  if (i > 0 && p.pub[i]) {
+    // downwind neighbour inside the local box: publish (its consumer runs one group later)
+    const int cd = c[i] - up;
+    if (cd >= 0 && cd < p.L[i]) out = kOutPub;
+  }
+  if (outside && p.xsplit[i]) {
+    // the upwind neighbour lives on another rank: its trace arrived in the halo buffer
+    src = kSrcHalo;
+    const int ls = p.lstride[i];
+    slot = p.hslot[i][(cell % ls) + (cell / (ls * p.L[i])) * ls];
+  } else if (i == 0) {
+    if (!p.pencil) {
+      src = kSrcGroup;
+      nb = k + (cn - c[0]);
+    } else {
+      const int kk = k + up;
+      if (kk >= 0 && kk < p.CT) {
+        src = kSrcGroup;
+        nb = kk;
+      } else if (gi > 0) {
+        src = kSrcCarry;
+      }
+    }
+  } else if (!p.pencil && nbcell >= first && nbcell < first + p.CT) {
+    src = kSrcGroup;
+    nb = nbcell - first;
+  } else if (p.pub[i] && !outside) {
+    // the producer: the unit holding the upwind neighbour; ready when it finished the step that
+    // processed the neighbour's group (the flag counts completed steps in this launch)
+    int cn2[kMaxD];
+#pragma unroll
+    for (int j = 0; j < kMaxD; ++j) cn2[j] = c[j];
+    cn2[i] = cn;
+    const int pu = unit_of<D>(p, cn2);
+    int pc[kMaxD], pt[kMaxD], pdir0, pskew;
+    pencil_decode<D>(p, pu, pc, pt, pdir0, pskew);
+    const int need = p.epoch | (group_step(p, c[0] / p.CT, pdir0, pskew) + 1);
+    if (ld_acquire(p.flags + pu) >= need) {
+      src = kSrcPub;
+      slot = pu;
+    }
+  }
+  ci.src[i] = src;
+  ci.out[i] = out;
+  ci.nb[i] = nb;
+  ci.slot[i] = slot;
 }
 
 // Cell-local offset (dim-X digit 0) of face point f = N r + l of dim X in the phase layout of X: rest
@@ -383,14 +391,13 @@ __device__ __forceinline__ void trace_global(const double *nb, int S, double (&t
   }
 }
 template <int D, int N, int SX, int SY>
-__device__ __forceinline__ void trace_smem(const double *cellbuf, int pR, int S, double (&t)[N]) {
+__device__ __forceinline__ void trace_smem(const double *cellbuf, int sR, int S, double (&t)[N]) {
   const double *tau = c_tab[N].tau[S];
-  const double *c = cellbuf + pR;
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    double s = tau[0] * c[phys<D, N>(l * SY)];
+    double s = tau[0] * cellbuf[sR ^ swz<D, N>(l * SY)];
 #pragma unroll
-    for (int j = 1; j < N; ++j) s = fma(tau[j], c[phys<D, N>(j * SX + l * SY)], s);
+    for (int j = 1; j < N; ++j) s = fma(tau[j], cellbuf[sR ^ swz<D, N>(j * SX + l * SY)], s);
     t[l] = s;
   }
 }
@@ -427,45 +434,36 @@ __device__ __forceinline__ void load_vec(const double *src, double (&t)[N], bool
   }
 }
 
-// Obtain the upwind trace of dim X for this thread (X is the tile's first index when FIRST_IDX, i.e.
-// X = P: lines along P, face points indexed by b; else X = Q).
-template <int D, int N, int SX, int SY, bool WS>
-__device__ __forceinline__ void upwind_trace(const CellParams &p, const CellInfo &ci, int X, int R, int pR, int r,
-                                             const double *Ugroup, const double *carry_in, const double *TRk,
-                                             double (&t)[N]) {
+// pointer to this thread's N values of the published / halo trace of dim X
+template <int D, int N>
+__device__ __forceinline__ const double *remote_trace(const CellParams &p, const CellInfo &ci, int X, int r) {
   using G = CGeo<D, N>;
-  const int S = ci.sg[X];
-  if constexpr (WS) {
-    // warp-specialised kernel: the loader warps staged every non-local trace in smem
-    const int src = ci.src[X];
-    if (src != kSrcGroup && src != kSrcCarry) {
-      load_vec<N>(TRk + X * G::FN + N * r, t, false);
-      return;
-    }
-  }
+  if (ci.src[X] == kSrcPub) return p.tbuf[X] + ((size_t)ci.slot[X] * p.UC + ci.cu) * G::FN + (size_t)N * r;
+  return p.hbuf[X] + (size_t)ci.slot[X] * G::FN + (size_t)N * r;
+}
+
+// Early part of the upwind trace of dim X: the sources that are a plain N-value load (carry, published,
+// halo). In-group (smem) and direct (global) traces are contracted after the passes.
+template <int D, int N, int SX, int SY>
+__device__ __forceinline__ void trace_early(const CellParams &p, const CellInfo &ci, int X, int sR, int r,
+                                            const double *Ugroup, const double *carry_in, double (&t)[N]) {
   switch (ci.src[X]) {
-    case kSrcGroup:
-      trace_smem<D, N, SX, SY>(Ugroup + (size_t)ci.nb[X] * cell_stride<D, N>(), pR, S, t);
-      break;
     case kSrcCarry:
       load_vec<N>(carry_in + N * r, t, false);
       break;
     case kSrcPub:
-      load_vec<N>(p.tbuf[X] + ((size_t)ci.slot[X] * p.UC + ci.cu) * G::FN + (size_t)N * r, t, true);
-      break;
     case kSrcHalo:
-      load_vec<N>(p.hbuf[X] + (size_t)ci.slot[X] * G::FN + (size_t)N * r, t, true);
+      load_vec<N>(remote_trace<D, N>(p, ci, X, r), t, true);
       break;
     default:
-      trace_global<D, N, SX, SY>(p.u + (size_t)ci.nb[X] * G::ND + R, S, t);
       break;
   }
 }
 
-template <int D, int N, int MODE, int PH, bool WS>
+template <int D, int N, int MODE, int PH>
 __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
                                           const double *Ug, double *ACC, const double *carry_in, double *carry_out,
-                                          const double *TRk, bool active) {
+                                          bool active) {
   if (!active) return;  // padding threads of the CTA: only the barriers between phases
   using G = CGeo<D, N>;
   constexpr int P = G::P(PH), Q = G::Q(PH);
@@ -477,16 +475,21 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   ThreadPhase tp;
   thread_phase<D, N, PH, LAST && MODE == kModeAdvection>(p, r, stab, stab + 8, tp);
   const int R = tp.R;
-  const int pR = phys<D, N>(R);
-  constexpr int CS = cell_stride<D, N>();
-  const double *U = Ug + (size_t)k * CS + pR;
-  double *A = ACC + (size_t)k * CS + pR;
+  const int sR = swz<D, N>(R);
+  const double *U = Ug + (size_t)k * G::ND;
+  double *A = ACC + (size_t)k * G::ND;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
   const size_t g0 = (size_t)ci.cell * G::ND + R;
   // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line (a_i varies only with the other dims)
   const double facP = p.dtfac * p.inv_h[P], facQ = p.dtfac * p.inv_h[Q];
   const double s0P = (ci.base[P] + tp.wP) * facP, slP = p.a_lin[P][Q] * p.h[Q] * facP;
   const double s0Q = (ci.base[Q] + tp.wQ) * facQ, slQ = p.a_lin[Q][P] * p.h[P] * facQ;
+
+  // upwind traces from smem / the published and halo buffers, issued before the passes (their L2
+  // latency hides behind the passes; the carry may then be overwritten in place by this pass)
+  double tP[N], tQ[N];
+  trace_early<D, N, SP, SQ>(p, ci, P, sR, r, Ug, carry_in, tP);
+  if constexpr (QA) trace_early<D, N, SQ, SP>(p, ci, Q, sR, r, Ug, carry_in, tQ);
 
   double acc[N][N];
   {
@@ -496,7 +499,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       for (int b = 0; b < N; ++b)
 #pragma unroll
         for (int a = 0; a < N; a += 2) {
-          const double2 v = *reinterpret_cast<const double2 *>(U + phys<D, N>(a + b * SQ));
+          const double2 v = *reinterpret_cast<const double2 *>(U + (sR ^ swz<D, N>(a + b * SQ)));
           uv[a][b] = v.x;
           uv[a + 1][b] = v.y;
         }
@@ -504,22 +507,23 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) uv[a][b] = U[phys<D, N>(a * SP + b * SQ)];
+        for (int b = 0; b < N; ++b) uv[a][b] = U[sR ^ swz<D, N>(a * SP + b * SQ)];
     }
     if constexpr (!FIRST) {
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) acc[a][b] = A[phys<D, N>(a * SP + b * SQ)];
+        for (int b = 0; b < N; ++b) acc[a][b] = A[sR ^ swz<D, N>(a * SP + b * SQ)];
     }
     if constexpr (LAST && MODE == kModeRK) {
       const unsigned long long pol = evict_first_policy();
       // dU of the tile -> this thread's own ACC positions (already consumed), asynchronously; read back
-      // in the epilogue, so its HBM latency overlaps the passes and the upwind-trace work
+      // in the epilogue, so its HBM latency overlaps the passes and the lifts
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) cp_async8_ef(A + phys<D, N>(a * SP + b * SQ), p.du + g0 + a * SP + b * SQ, pol);
+        for (int b = 0; b < N; ++b)
+          cp_async8_ef(A + (sR ^ swz<D, N>(a * SP + b * SQ)), p.du + g0 + a * SP + b * SQ, pol);
       cp_async_commit();
     }
     // volume terms of P and Q and this cell's downwind traces along P and Q
@@ -550,42 +554,56 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     }
   }
 
-  // upwind traces and rank-1 lifts
-  {
-    double t[N];
-    upwind_trace<D, N, SP, SQ, WS>(p, ci, P, R, pR, r, Ug, carry_in, TRk, t);
-    if (sgP == 0) {
+  // in-group neighbours (smem) and direct reads of the upwind neighbour (traces not published in time)
+  if (ci.src[P] == kSrcGroup) trace_smem<D, N, SP, SQ>(Ug + (size_t)ci.nb[P] * G::ND, sR, sgP, tP);
+  else if (ci.src[P] == kSrcDirect) trace_global<D, N, SP, SQ>(p.u + (size_t)ci.nb[P] * G::ND + R, sgP, tP);
+  if constexpr (QA) {
+    if (ci.src[Q] == kSrcGroup) trace_smem<D, N, SQ, SP>(Ug + (size_t)ci.nb[Q] * G::ND, sR, sgQ, tQ);
+    else if (ci.src[Q] == kSrcDirect) trace_global<D, N, SQ, SP>(p.u + (size_t)ci.nb[Q] * G::ND + R, sgQ, tQ);
+  }
+
+  // rank-1 lifts of the upwind traces
+  if (sgP == 0) {
 #pragma unroll
-      for (int b = 0; b < N; ++b) {
-        const double tb = t[b] * fma(slP, T.xi[b], s0P);
+    for (int b = 0; b < N; ++b) {
+      const double tb = tP[b] * fma(slP, T.xi[b], s0P);
 #pragma unroll
-        for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[0][a], tb, acc[a][b]);
-      }
-    } else {
+      for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[0][a], tb, acc[a][b]);
+    }
+  } else {
 #pragma unroll
-      for (int b = 0; b < N; ++b) {
-        const double tb = t[b] * fma(slP, T.xi[b], s0P);
+    for (int b = 0; b < N; ++b) {
+      const double tb = tP[b] * fma(slP, T.xi[b], s0P);
 #pragma unroll
-        for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[1][a], tb, acc[a][b]);
-      }
+      for (int a = 0; a < N; ++a) acc[a][b] = fma(T.lam[1][a], tb, acc[a][b]);
     }
   }
   if constexpr (QA) {
-    double t[N];
-    upwind_trace<D, N, SQ, SP, WS>(p, ci, Q, R, pR, r, Ug, carry_in, TRk, t);
     if (sgQ == 0) {
 #pragma unroll
       for (int a = 0; a < N; ++a) {
-        const double ta = t[a] * fma(slQ, T.xi[a], s0Q);
+        const double ta = tQ[a] * fma(slQ, T.xi[a], s0Q);
 #pragma unroll
         for (int b = 0; b < N; ++b) acc[a][b] = fma(T.lam[0][b], ta, acc[a][b]);
       }
     } else {
 #pragma unroll
       for (int a = 0; a < N; ++a) {
-        const double ta = t[a] * fma(slQ, T.xi[a], s0Q);
+        const double ta = tQ[a] * fma(slQ, T.xi[a], s0Q);
 #pragma unroll
         for (int b = 0; b < N; ++b) acc[a][b] = fma(T.lam[1][b], ta, acc[a][b]);
+      }
+    }
+  }
+  // published traces are consumed exactly once: drop their L2 lines without write-back (one lane per
+  // 128-byte line, after the whole warp has its values)
+  if constexpr ((N * 8) <= 128 && 128 % (N * 8) == 0) {
+    constexpr int TPL = 128 / (N * 8);  // threads per line
+    __syncwarp();
+    if (r % TPL == 0) {
+      if (ci.src[P] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, P, r));
+      if constexpr (QA) {
+        if (ci.src[Q] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, Q, r));
       }
     }
   }
@@ -594,7 +612,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int b = 0; b < N; ++b) A[phys<D, N>(a * SP + b * SQ)] = acc[a][b];
+      for (int b = 0; b < N; ++b) A[sR ^ swz<D, N>(a * SP + b * SQ)] = acc[a][b];
   } else if constexpr (MODE == kModeAdvection) {
     // weak form: v = M (M^-1 A u), M_qq = |J| prod_i w_{q_i}
     const double wr = tp.wr;
@@ -609,7 +627,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) {
-        const int o = phys<D, N>(a * SP + b * SQ);
+        const int o = sR ^ swz<D, N>(a * SP + b * SQ);
         double dun = acc[a][b];
         if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
         __stcs(p.du + g0 + a * SP + b * SQ, dun);
@@ -618,42 +636,28 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   }
 }
 
-// named barrier among the first `count` threads (warp multiples)
-__device__ __forceinline__ void bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
-}
-
 // One group (all phases). Not inlined into the persistent loop, so that group-invariant values are not
-// hoisted out of it and kept live in registers across the whole loop. WS: only the compute warps run it
-// (phase barrier = named barrier 5 over `ncompute` threads).
-#ifndef HD_PG_INLINE
-#define HD_PG_INLINE __noinline__
-#endif
-template <int D, int N, int MODE, bool WS>
-__device__ HD_PG_INLINE void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
+// hoisted out of it and kept live in registers across the whole loop.
+template <int D, int N, int MODE>
+__device__ __noinline__ void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
                                            const double *Ug, double *ACC, const double *carry_in, double *carry_out,
-                                           const double *TRk, bool active, int ncompute) {
+                                           bool active) {
   using G = CGeo<D, N>;
-  run_phase<D, N, MODE, 0, WS>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, TRk, active);
+  run_phase<D, N, MODE, 0>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
   if constexpr (G::NPH > 1) {
-    if constexpr (WS) bar_sync(5, ncompute);
-    else __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0), WS>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, TRk, active);
+    __syncthreads();
+    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
   }
   if constexpr (G::NPH > 2) {
-    if constexpr (WS) bar_sync(5, ncompute);
-    else __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0), WS>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, TRk, active);
+    __syncthreads();
+    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
   }
 }
 
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * cell_stride<D, N>() + 2 * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo);
+  return (3 * CT * G::ND + (CT > 1 ? 2 : 1) * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo);
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
@@ -663,11 +667,13 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  constexpr int CS = cell_stride<D, N>();
-  double *Ubuf[2] = {smem, smem + CT * CS};
-  double *ACC = smem + 2 * CT * CS;
-  double *carry[2] = {ACC + CT * CS, ACC + CT * CS + G::FN};
-  double *stab = carry[1] + G::FN;                           // xi[8], w[8]
+  double *Ubuf[2] = {smem, smem + CT * G::ND};
+  double *ACC = smem + 2 * CT * G::ND;
+  // carry of the dim-0 trace between consecutive groups: one buffer when CT == 1 (the same thread reads
+  // it before overwriting it), two alternating buffers otherwise
+  const int ncarry = CT > 1 ? 2 : 1;
+  double *carry0 = ACC + CT * G::ND;
+  double *stab = carry0 + ncarry * G::FN;                    // xi[8], w[8]
   CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);  // CT entries
   const int tid = threadIdx.x;
   const int k = tid / G::NT;
@@ -685,20 +691,17 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     if constexpr (G::ND % 2 == 0) {
       for (int i = tid; i < (total >> 1); i += blockDim.x) {
         const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
-        cp_async16(dst + kc * CS + phys<D, N>(x), src + e);
+        cp_async16(dst + kc * G::ND + swz<D, N>(x), src + e);
       }
     } else {
-      for (int i = tid; i < total; i += blockDim.x) {
-        const int kc = i / G::ND, x = i - kc * G::ND;
-        cp_async8(dst + kc * CS + phys<D, N>(x), src + i);
-      }
+      for (int i = tid; i < total; i += blockDim.x) cp_async8(dst + i, src + i);
     }
   };
 
   int u = blockIdx.x, gi = 0, it = 0;
   copy_group(group_first_cell<D>(p, u, 0), Ubuf[0]);
   cp_async_commit();
-  int prev_unit = -1;
+  int prev_unit = -1, prev_step = 0;
   while (u < p.nunits) {
     // next group (this unit or the first group of the next unit)
     int un = u, gn = gi + 1;
@@ -708,20 +711,24 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     }
     __syncthreads();  // previous group finished: info, carry and the other U buffer are free
     if (prev_unit >= 0 && tid == 0) {
-      // the previous unit's traces are all written (barrier above): publish it
+      // the previous group's traces are all written (barrier above): publish its progress
       __threadfence();
-      *(volatile int *)(p.flags + prev_unit) = p.epoch;
+      *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
     }
-    prev_unit = -1;
     if (un < p.nunits) copy_group(group_first_cell<D>(p, un, gn), Ubuf[(it + 1) & 1]);
     cp_async_commit();
-    if (tid < CT) decode_cell<D>(p, u, gi, tid, info[tid]);
+    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
+      const int kk = idx / D;
+      decode_cell<D>(p, u, gi, kk, info[kk], idx - kk * D);
+    }
     cp_async_wait<1>();
     __syncthreads();
     // every thread enters (the phases are separated by CTA barriers); padding threads idle inside
-    process_group<D, N, MODE, false>(p, info[active ? k : 0], stab, k, r, Ubuf[it & 1], ACC, carry[(gi + 1) & 1],
-                                     carry[gi & 1], nullptr, active, 0);
-    if (gn == 0 && p.pubany) prev_unit = u;
+    process_group<D, N, MODE>(p, info[active ? k : 0], stab, k, r, Ubuf[it & 1], ACC,
+                              carry0 + (ncarry > 1 ? ((gi + 1) & 1) : 0) * G::FN,
+                              carry0 + (ncarry > 1 ? (gi & 1) : 0) * G::FN, active);
+    prev_unit = p.pubany ? u : -1;
+    prev_step = gi;
     u = un;
     gi = gn;
     ++it;
@@ -731,167 +738,9 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     __syncthreads();
     if (tid == 0) {
       __threadfence();
-      *(volatile int *)(p.flags + prev_unit) = p.epoch;
+      *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
     }
   }
-}
-
-}  // namespace hd
-
-namespace hd {
-
-// ---------------------------------------------------------------------------------------------------
-// Warp-specialised variant (1 CTA per SM): NCW compute warps run the phases from shared memory only;
-// 4 loader warps run up to two groups ahead -- decode, cp.async of the group's cells, cp.async of the
-// published / halo traces, and the neighbour-read traces (coalesced L2 loads + contraction) into a
-// double-buffered trace buffer TR[stage][cell][dim][n^(d-1)]. Hand-off by named barriers:
-//   1 + s: FULL[s]  (loader arrives, compute syncs)     3 + s: EMPTY[s] (compute arrives, loader syncs)
-//   5: compute-internal phase barrier                    6: loader-internal barrier
-constexpr int kLoaderThreads = 128;
-
-template <int D, int N>
-__host__ __device__ constexpr int ws_smem_bytes(int CT) {
-  using G = CGeo<D, N>;
-  return (3 * CT * cell_stride<D, N>() + 2 * CT * D * G::FN + 2 * G::FN + 16) * 8 + 2 * CT * (int)sizeof(CellInfo);
-}
-
-template <int D, int N>
-__device__ __forceinline__ void ws_unit_group(const CellParams &p, int j, int &u, int &gi) {
-  // j-th group of this CTA's sequence
-  const int ju = j / p.GPU;
-  gi = j - ju * p.GPU;
-  u = blockIdx.x + ju * gridDim.x;
-}
-
-template <int D, int N, int MODE>
-__global__ void __launch_bounds__(HD_WS_LB, 1) cell_kernel_ws(const __grid_constant__ CellParams p) {
-  using G = CGeo<D, N>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int CT = p.CT;
-  const int NC = ((CT * G::NT + 31) / 32) * 32;  // compute threads
-  double *smem = reinterpret_cast<double *>(smem_raw);
-  constexpr int CS = cell_stride<D, N>();
-  double *Ubuf0 = smem;
-  double *ACC = smem + 2 * CT * CS;
-  double *TR0 = ACC + CT * CS;                          // [2][CT][D][FN]
-  double *carry0 = TR0 + 2 * CT * D * G::FN;            // [2][FN]
-  double *stab = carry0 + 2 * G::FN;                    // xi[8], w[8]
-  CellInfo *info0 = reinterpret_cast<CellInfo *>(stab + 16);  // [2][CT]
-  const int tid = threadIdx.x;
-  if (tid < 8) {
-    stab[tid] = tid < N ? c_tab[N].xi[tid] : 0.0;
-    stab[8 + tid] = tid < N ? c_tab[N].w[tid] : 0.0;
-  }
-  if ((int)blockIdx.x >= p.nunits) return;
-  __syncthreads();
-  const int my_units = (p.nunits - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int ngroups = my_units * p.GPU;
-  const int NTOT = NC + kLoaderThreads;
-
-  if (tid >= NC) {
-    // ------------------------------ loader warps ------------------------------
-    const int lt = tid - NC;
-    for (int j = 0; j < ngroups; ++j) {
-      const int s = j & 1;
-      int u, gi;
-      ws_unit_group<D, N>(p, j, u, gi);
-      if (j >= 2) bar_sync(3 + s, NTOT);  // compute finished group j-2: stage s is free
-      CellInfo *info = info0 + s * CT;
-      for (int k = lt; k < CT; k += kLoaderThreads) decode_cell<D>(p, u, gi, k, info[k]);
-      const int first = group_first_cell<D>(p, u, gi);
-      // the group's cells
-      {
-        double *dst = Ubuf0 + s * CT * CS;
-        const double *src = p.u + (size_t)first * G::ND;
-        const int total = CT * G::ND;
-        if constexpr (G::ND % 2 == 0) {
-          for (int i = lt; i < (total >> 1); i += kLoaderThreads) {
-            const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
-            cp_async16(dst + kc * CS + phys<D, N>(x), src + e);
-          }
-        } else {
-          for (int i = lt; i < total; i += kLoaderThreads) {
-            const int kc = i / G::ND, x = i - kc * G::ND;
-            cp_async8(dst + kc * CS + phys<D, N>(x), src + i);
-          }
-        }
-      }
-      bar_sync(6, kLoaderThreads);  // info visible to all loader threads
-      double *TR = TR0 + s * CT * D * G::FN;
-      // published / halo traces: plain copies (already in the phase layout)
-      for (int k = 0; k < CT; ++k) {
-        const CellInfo &ci = info[k];
-#pragma unroll
-        for (int X = 0; X < D; ++X) {
-          const int src = ci.src[X];
-          if (src != kSrcPub && src != kSrcHalo) continue;
-          const double *g = src == kSrcPub ? p.tbuf[X] + ((size_t)ci.slot[X] * p.UC + ci.cu) * G::FN
-                                           : p.hbuf[X] + (size_t)ci.slot[X] * G::FN;
-          double *d = TR + (k * D + X) * G::FN;
-          if constexpr (G::FN % 2 == 0) {
-            for (int i = lt; i < G::FN / 2; i += kLoaderThreads) cp_async16(d + 2 * i, g + 2 * i);
-          } else {
-            for (int i = lt; i < G::FN; i += kLoaderThreads) cp_async8(d + i, g + i);
-          }
-        }
-      }
-      cp_async_commit();
-      // neighbour-read traces: face points distributed with the lowest rest digit fastest (coalesced)
-      for (int k = 0; k < CT; ++k) {
-        const CellInfo &ci = info[k];
-#pragma unroll
-        for (int X = 0; X < D; ++X) {
-          if (ci.src[X] != kSrcDirect) continue;
-          constexpr int NR = G::FN / N;
-          const double *tau = c_tab[N].tau[ci.sg[X]];
-          const double *nb = p.u + (size_t)ci.nb[X] * G::ND;
-          int sx = 1;
-          for (int q = 0; q < X; ++q) sx *= N;
-          double *d = TR + (k * D + X) * G::FN;
-          for (int f2 = lt; f2 < G::FN; f2 += kLoaderThreads) {
-            const int l = f2 / NR, rr = f2 - l * NR;
-            const int f = rr * N + l;
-            const double *src = nb + face_offset<D, N>(X, f);
-            double v[N];
-#pragma unroll
-            for (int q = 0; q < N; ++q) v[q] = __ldg(src + q * sx);
-            double acc = tau[0] * v[0];
-#pragma unroll
-            for (int q = 1; q < N; ++q) acc = fma(tau[q], v[q], acc);
-            d[f] = acc;
-          }
-        }
-      }
-      cp_async_wait<0>();
-      bar_arrive(1 + s, NTOT);  // stage s full
-    }
-    return;
-  }
-
-  // ------------------------------ compute warps ------------------------------
-  const int k = tid / G::NT;
-  const int r = tid - k * G::NT;
-  const bool active = k < CT;
-  for (int j = 0; j < ngroups; ++j) {
-    const int s = j & 1;
-    int u, gi;
-    ws_unit_group<D, N>(p, j, u, gi);
-    bar_sync(1 + s, NTOT);  // wait for stage s
-    const CellInfo *info = info0 + s * CT;
-    const double *Ug = Ubuf0 + s * CT * CS;
-    const double *TRk = TR0 + (s * CT + (active ? k : 0)) * D * G::FN;
-    process_group<D, N, MODE, true>(p, info[active ? k : 0], stab, k, r, Ug, ACC, carry0 + ((gi + 1) & 1) * G::FN,
-                                    carry0 + (gi & 1) * G::FN, TRk, active, NC);
-    // all compute threads are done with stage s, ACC and the carry of this group
-    bar_sync(5, NC);
-    if (j + 2 < ngroups) bar_arrive(3 + s, NTOT);
-    if (gi == p.GPU - 1 && p.pubany && tid == 0) {
-      // the unit's published traces are all written (barrier above): publish the unit
-      __threadfence();
-      *(volatile int *)(p.flags + u) = p.epoch;
-    }
-  }
-  cp_async_wait<0>();
 }
 
 }  // namespace hd

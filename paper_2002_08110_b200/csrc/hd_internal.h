@@ -62,7 +62,7 @@ struct CellParams {
   double *out;            // A-mode: v; RK-mode: U_new
   double *du;             // RK-mode: dU (read unless first stage, written)
   int mode;
-  int epoch;              // unit-flag value that marks "complete in this launch"
+  int epoch;              // launch epoch << 10: a unit flag holds epoch | (groups completed in this launch)
   double rk_a, rk_b;      // stage coefficients A_s, B_s
   double dtfac;           // 1 (A-mode) or dt (RK-mode): folded into the line speeds
   double jdet;            // |J| = prod h_i
@@ -72,15 +72,13 @@ struct CellParams {
   int UC;                 // cells per unit (trace-buffer slot size)
   int pencil;             // 1: pencil mode
   int pubany;             // some dim publishes traces (unit flags needed)
-  int ws;                 // 1: warp-specialised kernel (loader warps stage all non-local traces)
   int L[kMaxD];           // cells per dim (local box)
   int lstride[kMaxD];     // cell-index stride per dim (memory order)
   int ustride[kMaxD];     // unit-index stride per dim (pencil mode, dims >= 1)
   double lo[kMaxD], h[kMaxD], inv_h[kMaxD];
   double a_const[kMaxD];
   double a_lin[kMaxD][kMaxD];
-  int pub[kMaxD];         // 1: dim publishes traces into tbuf (far buffer, one slot per unit)
-  int dirneg[kMaxD];      // published dims: traversal reversed (a_i < 0 on the whole box)
+  int pub[kMaxD];         // 1: dim publishes traces into tbuf (one slot per unit) for its downwind neighbour
   int follow[kMaxD];      // pencil mode, dims >= 1: traversal follows the sign of a_i (depends on slower dims only)
   int skew;               // pencil mode: skewed pencil start (see pencil_decode)
   double *tbuf[kMaxD];    // trace storage per dim: [unit][cell in unit][n^(d-1)]
@@ -132,9 +130,9 @@ bool cell_kernel_supported(int d, int n);
 // Kernel geometry for (d, n) on a local box with L0 cells along dim 0 and ncells cells: cells per group
 // CT, pencil mode, threads per CTA, dynamic smem bytes, phases.
 struct CellGeometry {
-  int CT, pencil, GPU, threads, smem, phases, ws;
+  int CT, pencil, GPU, threads, smem, phases;
 };
-CellGeometry cell_geometry(int d, int n, int L0, long long ncells, int ws);
+CellGeometry cell_geometry(int d, int n, int L0, long long ncells);
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd
@@ -159,7 +157,7 @@ struct hd_mesh {
   // trace machinery (device buffers owned by the mesh)
   hd::CellGeometry geo;
   int nunits;
-  int pub[6], dirneg[6];
+  int pub[6], follow[6];
   double *tbuf[6];
   int *flags;
   long long epoch;

@@ -202,14 +202,13 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 namespace {
 
 template <int D, int N>
-CellGeometry geometry_dn(int L0, long long ncells, int ws) {
+CellGeometry geometry_dn(int L0, long long ncells) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
-  g.ws = ws;
   const int maxCT = 256 / G::NT;
-  const int kSmemMax = ws ? 227 * 1024 : 113 * 1024;
-  auto smem_of = [&](int c) { return ws ? ws_smem_bytes<D, N>(c) : cell_smem_bytes<D, N>(c); };
+  const int kSmemMax = HD_MINB > 1 ? 113 * 1024 : 227 * 1024;
+  auto smem_of = [&](int c) { return cell_smem_bytes<D, N>(c); };
   if (L0 <= maxCT) {
     // multi-pencil groups: m whole pencils per group
     const long long npen = ncells / L0;
@@ -227,14 +226,14 @@ CellGeometry geometry_dn(int L0, long long ncells, int ws) {
     g.pencil = 1;
     g.GPU = L0 / CT;
   }
-  g.threads = ((g.CT * G::NT + 31) / 32) * 32 + (ws ? kLoaderThreads : 0);
+  g.threads = ((g.CT * G::NT + 31) / 32) * 32;
   g.smem = smem_of(g.CT);
   return g;
 }
 
 template <int D, int N, int MODE>
 cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
-  auto kern = g.ws ? cell_kernel_ws<D, N, MODE> : cell_kernel<D, N, MODE>;
+  auto kern = cell_kernel<D, N, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
   if (e != cudaSuccess) return e;
   int occ = 0;
@@ -246,11 +245,10 @@ cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
 
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
-  const CellGeometry g = geometry_dn<D, N>(p.L[0], (long long)p.nunits * p.UC, p.ws);
+  const CellGeometry g = geometry_dn<D, N>(p.L[0], (long long)p.nunits * p.UC);
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
-  if (p.ws) cell_kernel_ws<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
-  else cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -366,8 +364,8 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s
   HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0, long long ncells, int ws) {
-  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, ncells, ws)
+CellGeometry cell_geometry(int d, int n, int L0, long long ncells) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, ncells)
 }
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
   HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)
