@@ -1,6 +1,7 @@
 // hd_api.cpp -- the C ABI (include/hd.h): validation, mesh/partition plan, LSRK(5,4) driver.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -144,8 +145,12 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
     p.pubany |= m->pub[i];
   }
   p.flags = m->flags;
-  p.skew = g.pencil && g.GPU > 1 ? 1 : 0;
-  if (const char *e = getenv("HD_SKEW")) p.skew = p.skew && atoi(e) != 0;
+  // skew (steps a same-round producer runs ahead of its consumer): 2 gives the producer a full step of
+  // margin; the first `skew` steps of a pencil then read their upwind neighbours directly
+  p.skew = g.pencil && g.GPU > 2 ? 2 : (g.pencil && g.GPU > 1 ? 1 : 0);
+  if (const char *e = getenv("HD_SKEW")) p.skew = g.pencil ? std::min(atoi(e), g.GPU - 1) : 0;
+  p.discard = 1;
+  if (const char *e = getenv("HD_DISCARD")) p.discard = atoi(e) != 0;
   next_epoch(m, p, nullptr);
 }
 

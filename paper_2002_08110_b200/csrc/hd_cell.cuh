@@ -23,6 +23,12 @@
 #ifndef HD_MINB
 #define HD_MINB 1
 #endif
+#ifndef HD_PG_INLINE
+#define HD_PG_INLINE __forceinline__
+#endif
+#ifndef HD_DU_HINT
+#define HD_DU_HINT 0  // the L2::cache_hint form of cp.async faulted (illegal instruction) in the 6D RK kernel
+#endif
 
 namespace hd {
 
@@ -56,6 +62,17 @@ __host__ __device__ __forceinline__ constexpr int swz(int x) {
   }
 }
 
+// element T (disjoint digit fields from the thread's rest offset R, sR = swz(R)) of a cell buffer:
+// XOR of swizzled fields when n is a power of two (digits are bit fields), plain sum otherwise
+template <int D, int N>
+__device__ __forceinline__ constexpr int sidx(int sR, int T) {
+  if constexpr ((N & (N - 1)) == 0) {
+    return sR ^ swz<D, N>(T);
+  } else {
+    return sR + T;
+  }
+}
+
 struct CellInfo {
   double base[kMaxD];        // a_i at the cell's lower corner
   int cell;                  // local memory index of the cell
@@ -67,6 +84,14 @@ struct CellInfo {
   unsigned char out[kMaxD];  // TraceOut of the downwind trace per dim
   unsigned char sg[kMaxD];   // 1: a_i < 0 on this cell (upwind neighbour at +e_i)
   unsigned char pad[2];
+};
+
+// Pencil-mode decode of one unit, cached in smem for all its groups (pencil_decode, plus for each
+// published dim the producer unit of the upwind neighbours and its direction / start).
+struct UnitInfo {
+  int c[kMaxD], t[kMaxD];
+  int base, dir0, skew;
+  int pu[kMaxD], pdir0[kMaxD], pskew[kMaxD];
 };
 
 // per-thread, per-phase constants
@@ -103,8 +128,8 @@ __device__ __forceinline__ void cell_speed(const CellParams &p, int i, const int
 // that "follows" its speed (the sign of a_j depends only on slower dims, so it is constant along the
 // sweep) is traversed upwind -> downwind: c_j = L_j - 1 - t_j where a_j < 0. Then every upwind neighbour
 // along such a dim is an EARLIER unit. Returns the pencil's base cell, the dim-0 direction (1: a_0 < 0,
-// groups from the far end) and the skew: the pencil starts at group (-sum_j t_j) mod GPU, so a unit's
-// upwind neighbours along every dim (same round) are exactly one group ahead of it.
+// groups from the far end) and the start: the pencil starts at group (-K sum_j t_j) mod GPU (K = p.skew),
+// so a unit's upwind neighbours along every dim (same round) run K groups ahead of it.
 template <int D>
 __device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c)[kMaxD], int (&t)[kMaxD], int &dir0,
                                              int &skew) {
@@ -129,7 +154,7 @@ __device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c
   }
   double b0;
   cell_speed<D>(p, 0, c, b0, dir0);
-  skew = p.skew ? (p.GPU - tsum % p.GPU) % p.GPU : 0;
+  skew = (p.GPU - (p.skew * tsum) % p.GPU) % p.GPU;
   return base;
 }
 
@@ -163,34 +188,62 @@ __device__ __forceinline__ int group_step(const CellParams &p, int g, int dir0, 
   return (gg - skew + p.GPU) % p.GPU;
 }
 
-// First cell (memory order) of group gi of unit u.
+// Unit decode for the cache: thread j computes the unit (redundantly) and, for a published dim j, its
+// producer unit; thread 0 writes the unit fields.
 template <int D>
-__device__ __forceinline__ int group_first_cell(const CellParams &p, int u, int gi) {
-  if (!p.pencil) return u * p.CT;
+__device__ __forceinline__ void decode_unit(const CellParams &p, int u, int j, UnitInfo &ui) {
   int c[kMaxD], t[kMaxD], dir0, skew;
   const int base = pencil_decode<D>(p, u, c, t, dir0, skew);
-  return base + step_group(p, gi, dir0, skew) * p.CT;
+  if (j == 0) {
+#pragma unroll
+    for (int q = 0; q < kMaxD; ++q) {
+      ui.c[q] = c[q];
+      ui.t[q] = t[q];
+    }
+    ui.base = base;
+    ui.dir0 = dir0;
+    ui.skew = skew;
+  }
+  if (j >= 1 && j < D && p.pub[j]) {
+    // the upwind neighbour along j of every cell of this pencil sits in one pencil (a_j does not
+    // depend on z_0 or z_j): its unit, direction and start
+    double b;
+    int sg;
+    cell_speed<D>(p, j, c, b, sg);
+    int cn[kMaxD];
+#pragma unroll
+    for (int q = 0; q < kMaxD; ++q) cn[q] = c[q];
+    cn[j] = c[j] + (sg ? 1 : -1);
+    int pu = -1, pd = 0, ps = 0;
+    if (cn[j] >= 0 && cn[j] < p.L[j]) {
+      pu = unit_of<D>(p, cn);
+      int pc[kMaxD], pt[kMaxD];
+      pencil_decode<D>(p, pu, pc, pt, pd, ps);
+      if (pu >= u) pu = -1;  // not an earlier unit (a dim that does not follow): never published in time
+    }
+    ui.pu[j] = pu;
+    ui.pdir0[j] = pd;
+    ui.pskew[j] = ps;
+  }
 }
 
 // Decode dim `i` of cell k of group gi of unit u (dim 0 also writes the cell-level fields).
 template <int D>
-__device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, int k, CellInfo &ci, int i) {
-  int c[kMaxD], t[kMaxD];
+__device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo &ui, int u, int gi, int k, CellInfo &ci,
+                                            int i) {
+  int c[kMaxD];
   int first;
   if (p.pencil) {
-    int dir0, skew;
-    const int base = pencil_decode<D>(p, u, c, t, dir0, skew);
-    const int g = step_group(p, gi, dir0, skew);
+#pragma unroll
+    for (int j = 0; j < kMaxD; ++j) c[j] = ui.c[j];
+    const int g = step_group(p, gi, ui.dir0, ui.skew);
     c[0] = g * p.CT + k;
-    first = base + g * p.CT;
+    first = ui.base + g * p.CT;
   } else {
     first = u * p.CT;
     int rr = first + k;
 #pragma unroll
-    for (int j = 0; j < kMaxD; ++j) {
-      c[j] = 0;
-      t[j] = 0;
-    }
+    for (int j = 0; j < kMaxD; ++j) c[j] = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       c[j] = rr % p.L[j];
@@ -224,7 +277,7 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, 
     if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
   }
   if (i > 0 && p.pub[i]) {
-    // downwind neighbour inside the local box: publish (its consumer runs one group later)
+    // downwind neighbour inside the local box: publish (its consumer runs a few groups later)
     const int cd = c[i] - up;
     if (cd >= 0 && cd < p.L[i]) out = kOutPub;
   }
@@ -249,17 +302,11 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, int u, int gi, 
   } else if (!p.pencil && nbcell >= first && nbcell < first + p.CT) {
     src = kSrcGroup;
     nb = nbcell - first;
-  } else if (p.pub[i] && !outside) {
-    // the producer: the unit holding the upwind neighbour; ready when it finished the step that
-    // processed the neighbour's group (the flag counts completed steps in this launch)
-    int cn2[kMaxD];
-#pragma unroll
-    for (int j = 0; j < kMaxD; ++j) cn2[j] = c[j];
-    cn2[i] = cn;
-    const int pu = unit_of<D>(p, cn2);
-    int pc[kMaxD], pt[kMaxD], pdir0, pskew;
-    pencil_decode<D>(p, pu, pc, pt, pdir0, pskew);
-    const int need = p.epoch | (group_step(p, c[0] / p.CT, pdir0, pskew) + 1);
+  } else if (p.pub[i] && !outside && ui.pu[i] >= 0) {
+    // the producer finished the step that processed the neighbour's group (the flag counts the steps
+    // completed in this launch)?
+    const int pu = ui.pu[i];
+    const int need = p.epoch | (group_step(p, c[0] / p.CT, ui.pdir0[i], ui.pskew[i]) + 1);
     if (ld_acquire(p.flags + pu) >= need) {
       src = kSrcPub;
       slot = pu;
@@ -395,9 +442,9 @@ __device__ __forceinline__ void trace_smem(const double *cellbuf, int sR, int S,
   const double *tau = c_tab[N].tau[S];
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    double s = tau[0] * cellbuf[sR ^ swz<D, N>(l * SY)];
+    double s = tau[0] * cellbuf[sidx<D, N>(sR, l * SY)];
 #pragma unroll
-    for (int j = 1; j < N; ++j) s = fma(tau[j], cellbuf[sR ^ swz<D, N>(j * SX + l * SY)], s);
+    for (int j = 1; j < N; ++j) s = fma(tau[j], cellbuf[sidx<D, N>(sR, j * SX + l * SY)], s);
     t[l] = s;
   }
 }
@@ -499,7 +546,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       for (int b = 0; b < N; ++b)
 #pragma unroll
         for (int a = 0; a < N; a += 2) {
-          const double2 v = *reinterpret_cast<const double2 *>(U + (sR ^ swz<D, N>(a + b * SQ)));
+          const double2 v = *reinterpret_cast<const double2 *>(U + sidx<D, N>(sR, a + b * SQ));
           uv[a][b] = v.x;
           uv[a + 1][b] = v.y;
         }
@@ -507,13 +554,13 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) uv[a][b] = U[sR ^ swz<D, N>(a * SP + b * SQ)];
+        for (int b = 0; b < N; ++b) uv[a][b] = U[sidx<D, N>(sR, a * SP + b * SQ)];
     }
     if constexpr (!FIRST) {
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) acc[a][b] = A[sR ^ swz<D, N>(a * SP + b * SQ)];
+        for (int b = 0; b < N; ++b) acc[a][b] = A[sidx<D, N>(sR, a * SP + b * SQ)];
     }
     if constexpr (LAST && MODE == kModeRK) {
       const unsigned long long pol = evict_first_policy();
@@ -523,7 +570,8 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int b = 0; b < N; ++b)
-          cp_async8_ef(A + (sR ^ swz<D, N>(a * SP + b * SQ)), p.du + g0 + a * SP + b * SQ, pol);
+          if constexpr (HD_DU_HINT) cp_async8_ef(A + sidx<D, N>(sR, a * SP + b * SQ), p.du + g0 + a * SP + b * SQ, pol);
+          else cp_async8(A + sidx<D, N>(sR, a * SP + b * SQ), p.du + g0 + a * SP + b * SQ);
       cp_async_commit();
     }
     // volume terms of P and Q and this cell's downwind traces along P and Q
@@ -600,7 +648,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   if constexpr ((N * 8) <= 128 && 128 % (N * 8) == 0) {
     constexpr int TPL = 128 / (N * 8);  // threads per line
     __syncwarp();
-    if (r % TPL == 0) {
+    if (p.discard && r % TPL == 0) {
       if (ci.src[P] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, P, r));
       if constexpr (QA) {
         if (ci.src[Q] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, Q, r));
@@ -612,7 +660,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int b = 0; b < N; ++b) A[sR ^ swz<D, N>(a * SP + b * SQ)] = acc[a][b];
+      for (int b = 0; b < N; ++b) A[sidx<D, N>(sR, a * SP + b * SQ)] = acc[a][b];
   } else if constexpr (MODE == kModeAdvection) {
     // weak form: v = M (M^-1 A u), M_qq = |J| prod_i w_{q_i}
     const double wr = tp.wr;
@@ -627,7 +675,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) {
-        const int o = sR ^ swz<D, N>(a * SP + b * SQ);
+        const int o = sidx<D, N>(sR, a * SP + b * SQ);
         double dun = acc[a][b];
         if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
         __stcs(p.du + g0 + a * SP + b * SQ, dun);
@@ -639,7 +687,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 // One group (all phases). Not inlined into the persistent loop, so that group-invariant values are not
 // hoisted out of it and kept live in registers across the whole loop.
 template <int D, int N, int MODE>
-__device__ __noinline__ void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
+__device__ HD_PG_INLINE void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
                                            const double *Ug, double *ACC, const double *carry_in, double *carry_out,
                                            bool active) {
   using G = CGeo<D, N>;
@@ -657,7 +705,8 @@ __device__ __noinline__ void process_group(const CellParams &p, const CellInfo &
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * G::ND + (CT > 1 ? 2 : 1) * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo);
+  return (3 * CT * G::ND + (CT > 1 ? 2 : 1) * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo) +
+         2 * (int)sizeof(UnitInfo);
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
@@ -667,14 +716,14 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  double *Ubuf[2] = {smem, smem + CT * G::ND};
-  double *ACC = smem + 2 * CT * G::ND;
+  double *ACC = smem + 2 * CT * G::ND;  // U double buffer: smem + (it & 1) * CT * ND
   // carry of the dim-0 trace between consecutive groups: one buffer when CT == 1 (the same thread reads
   // it before overwriting it), two alternating buffers otherwise
   const int ncarry = CT > 1 ? 2 : 1;
   double *carry0 = ACC + CT * G::ND;
   double *stab = carry0 + ncarry * G::FN;                    // xi[8], w[8]
   CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);  // CT entries
+  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info + CT);  // 2 entries
   const int tid = threadIdx.x;
   const int k = tid / G::NT;
   const int r = tid - k * G::NT;
@@ -698,8 +747,19 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     }
   };
 
-  int u = blockIdx.x, gi = 0, it = 0;
-  copy_group(group_first_cell<D>(p, u, 0), Ubuf[0]);
+  // unit-decode cache: slot (j & 1) holds this CTA's j-th unit; the next unit is decoded while the
+  // current one starts (its first group's cells are prefetched during the current unit's last group)
+  int u = blockIdx.x, gi = 0, it = 0, ju = 0;
+  if (p.pencil) {
+    if (tid < D) decode_unit<D>(p, u, tid, uinfo[0]);
+    if (tid >= 32 && tid < 32 + D && u + (int)gridDim.x < p.nunits)
+      decode_unit<D>(p, u + gridDim.x, tid - 32, uinfo[1]);
+    __syncthreads();
+  }
+  auto first_cell = [&](int uu, int g, const UnitInfo &ui) {
+    return p.pencil ? ui.base + step_group(p, g, ui.dir0, ui.skew) * CT : uu * CT;
+  };
+  copy_group(first_cell(u, 0, uinfo[0]), smem);
   cp_async_commit();
   int prev_unit = -1, prev_step = 0;
   while (u < p.nunits) {
@@ -715,20 +775,28 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       __threadfence();
       *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
     }
-    if (un < p.nunits) copy_group(group_first_cell<D>(p, un, gn), Ubuf[(it + 1) & 1]);
+    if (p.pencil && gi == 0 && ju > 0) {
+      // decode the next unit into the slot the previous unit used
+      const int u2 = u + gridDim.x;
+      if (tid < D && u2 < p.nunits) decode_unit<D>(p, u2, tid, uinfo[(ju + 1) & 1]);
+      if (p.GPU == 1) __syncthreads();  // needed right below by the prefetch
+    }
+    if (un < p.nunits) copy_group(first_cell(un, gn, uinfo[(ju + (gn == 0 ? 1 : 0)) & 1]),
+                                  smem + ((it + 1) & 1) * CT * G::ND);
     cp_async_commit();
     for (int idx = tid; idx < CT * D; idx += blockDim.x) {
       const int kk = idx / D;
-      decode_cell<D>(p, u, gi, kk, info[kk], idx - kk * D);
+      decode_cell<D>(p, uinfo[ju & 1], u, gi, kk, info[kk], idx - kk * D);
     }
     cp_async_wait<1>();
     __syncthreads();
     // every thread enters (the phases are separated by CTA barriers); padding threads idle inside
-    process_group<D, N, MODE>(p, info[active ? k : 0], stab, k, r, Ubuf[it & 1], ACC,
+    process_group<D, N, MODE>(p, info[active ? k : 0], stab, k, r, smem + (it & 1) * CT * G::ND, ACC,
                               carry0 + (ncarry > 1 ? ((gi + 1) & 1) : 0) * G::FN,
                               carry0 + (ncarry > 1 ? (gi & 1) : 0) * G::FN, active);
     prev_unit = p.pubany ? u : -1;
     prev_step = gi;
+    if (gn == 0) ++ju;
     u = un;
     gi = gn;
     ++it;

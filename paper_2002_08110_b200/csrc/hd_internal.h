@@ -80,7 +80,8 @@ struct CellParams {
   double a_lin[kMaxD][kMaxD];
   int pub[kMaxD];         // 1: dim publishes traces into tbuf (one slot per unit) for its downwind neighbour
   int follow[kMaxD];      // pencil mode, dims >= 1: traversal follows the sign of a_i (depends on slower dims only)
-  int skew;               // pencil mode: skewed pencil start (see pencil_decode)
+  int skew;               // pencil mode: a pencil starts at group (-skew * sum_j t_j) mod GPU (pencil_decode)
+  int discard;            // drop consumed published-trace lines from L2 (no write-back)
   double *tbuf[kMaxD];    // trace storage per dim: [unit][cell in unit][n^(d-1)]
   int *flags;             // [nunits] unit completion flags (value = epoch)
   // multi-rank: the local box starts at global cell coordinates coff; along a split x dim

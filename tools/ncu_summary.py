@@ -54,3 +54,20 @@ data.sort(key=lambda r: -int(r[iss] or 0))
 print("top stall lines")
 for r in data[:top]:
     print(f"  {int(r[iss]) / max(tot_s, 1) * 100:5.1f}%  {r[0][-5:]}  {r[isrc][:70]}")
+
+# per CUDA source line (needs -lineinfo)
+try:
+    src2 = list(csv.reader(io.StringIO(run(["--page", "source", "--csv", "--print-source", "cuda"]))))
+    h3 = src2[1] if len(src2) > 1 else []
+    if "Warp Stall Sampling (All Samples)" in h3:
+        i_s = h3.index("Warp Stall Sampling (All Samples)")
+        i_l = h3.index("Line") if "Line" in h3 else 0
+        i_src = h3.index("Source")
+        rows = [r for r in src2[2:] if len(r) > i_s and r[i_s]]
+        tot3 = sum(int(r[i_s]) for r in rows) or 1
+        rows.sort(key=lambda r: -int(r[i_s]))
+        print("top CUDA lines by stall samples")
+        for r in rows[:top]:
+            print(f"  {int(r[i_s]) / tot3 * 100:5.1f}%  L{r[i_l]:>5s}  {r[i_src].strip()[:90]}")
+except Exception as ex:  # older ncu: no cuda view
+    print("no CUDA-line view:", ex)
