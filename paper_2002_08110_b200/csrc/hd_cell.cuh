@@ -647,8 +647,12 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   // 128-byte line, after the whole warp has its values)
   if constexpr ((N * 8) <= 128 && 128 % (N * 8) == 0) {
     constexpr int TPL = 128 / (N * 8);  // threads per line
-    __syncwarp();
-    if (p.discard && r % TPL == 0) {
+    if (p.discard && p.pubany) {
+      // lanes of this warp that run the phase (padding threads k >= CT returned at the top)
+      const int wb = (int)(threadIdx.x & ~31u), nact = p.CT * G::NT - wb;
+      __syncwarp(nact >= 32 ? 0xffffffffu : ((1u << nact) - 1u));
+    }
+    if (p.discard && p.pubany && r % TPL == 0) {
       if (ci.src[P] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, P, r));
       if constexpr (QA) {
         if (ci.src[Q] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, Q, r));
