@@ -56,7 +56,7 @@ typedef enum {
 
 typedef struct {
   int d_x, d_v;         /* space dims, 1..3 each; d = d_x + d_v in 2..6 */
-  int k;                /* polynomial degree; n = k+1 in 2..6; (n,d) must satisfy n^d <= 7776 */
+  int k;                /* polynomial degree; n = k+1 in 2..6; n^d must be <= 4096 on the GPU path */
   long long cells[6];   /* cells per dim, x dims first; all >= 1 */
   double lo[6], hi[6];  /* box per dim, hi > lo; periodic in every dim (C9) */
   double a_const[6];    /* advection field a_i(z) = a_const[i] + sum_j a_lin[i][j] z_j ...   */

@@ -116,7 +116,8 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.CT = g.CT;
   p.GPU = g.GPU;
   p.pencil = g.pencil;
-  p.UC = g.pencil ? (int)m->pt.len[0] : g.CT;
+  p.UC = g.pencil ? (int)m->pt.len[0] * g.CT : g.CT;
+  p.FN = (int)(m->nd / m->n);
   p.nunits = m->nunits;
   p.jdet = m->jdet;
   int lstride = 1, ustride = 1;
@@ -132,7 +133,7 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
     lstride *= p.L[i];
     if (i >= 1) {
       p.ustride[i] = ustride;
-      ustride *= p.L[i];
+      ustride *= i == 1 && g.pencil ? p.L[i] / g.CT : p.L[i];
     }
     p.lo[i] = m->desc.lo[i];
     p.h[i] = m->h[i];
@@ -467,8 +468,8 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     delete m;
     return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
   }
-  m->geo = hd::cell_geometry(d, n, (int)pt.len[0], m->ncells_local);
-  m->nunits = (int)(m->geo.pencil ? m->ncells_local / pt.len[0] : m->ncells_local / m->geo.CT);
+  m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local);
+  m->nunits = (int)(m->geo.pencil ? m->ncells_local / (pt.len[0] * m->geo.CT) : m->ncells_local / m->geo.CT);
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
   if (e != cudaSuccess) {
     delete m;

@@ -45,7 +45,8 @@ struct CGeo {
   static constexpr __host__ __device__ int P(int ph) { return ph == 0 ? 0 : 2 * ph - 1; }
   static constexpr __host__ __device__ int Q(int ph) { return ph == 0 ? D - 1 : 2 * ph; }
   static constexpr __host__ __device__ bool QA(int ph) { return ph == 0 || 2 * ph != D - 1; }
-  static constexpr bool OK = NT <= 256 && (3 * ND + 2 * FN + 16) * 8 + 256 <= 227 * 1024;
+  // one cell must fit the smem pipeline (cell_smem_bytes with CT = 1): n^d <= 4096
+  static constexpr bool OK = NT <= 256 && (5 * ND + NPH * 2 * FN + FN + 16) * 8 + 1024 <= 227 * 1024;
 };
 
 // Shared-memory element order of a cell (n = 4, d >= 4): XOR swizzle of bits 1..3 with bits 4, 6, 7.
@@ -79,7 +80,8 @@ struct CellInfo {
   int cu;                    // cell slot inside its unit (trace-buffer addressing)
   int unit;                  // the unit being processed (kOutPub slot)
   int nb[kMaxD];             // kSrcDirect: neighbour cell index; kSrcGroup: neighbour slot k' in the group
-  int slot[kMaxD];           // kSrcPub: producer unit; kSrcHalo: receive slot
+  int slot[kMaxD];           // kSrcPub: producer trace index (unit * UC + cell slot); kSrcHalo: receive slot
+  const double *tsrc[kMaxD]; // kSrcPub / kSrcHalo: the trace to stage in smem (else null)
   unsigned char src[kMaxD];  // TraceSrc of the upwind trace per dim
   unsigned char out[kMaxD];  // TraceOut of the downwind trace per dim
   unsigned char sg[kMaxD];   // 1: a_i < 0 on this cell (upwind neighbour at +e_i)
@@ -124,6 +126,8 @@ __device__ __forceinline__ void cell_speed(const CellParams &p, int i, const int
   sg = (ab + half) < 0.0 ? 1 : 0;
 }
 
+// Pencil mode: a group is CT cells at the same c_0 from CT adjacent pencils (along dim 1); a unit is those
+// CT pencils, processed one c_0 position (group) per step.
 // Pencil-mode unit decode, slowest dim first: traversal coordinates t_j = (u / ustride_j) % L_j; a dim
 // that "follows" its speed (the sign of a_j depends only on slower dims, so it is constant along the
 // sweep) is traversed upwind -> downwind: c_j = L_j - 1 - t_j where a_j < 0. Then every upwind neighbour
@@ -141,7 +145,9 @@ __device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c
   }
 #pragma unroll
   for (int j = D - 1; j >= 1; --j) {
-    const int tj = (u / p.ustride[j]) % p.L[j];
+    // dim 1 is traversed in blocks of CT cells (the cells of one group)
+    const int ext = j == 1 ? p.L[1] / p.CT : p.L[j];
+    const int tj = (u / p.ustride[j]) % ext;
     t[j] = tj;
     tsum += tj;
     int neg = 0;
@@ -149,7 +155,8 @@ __device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c
       double b;
       cell_speed<D>(p, j, c, b, neg);  // faster coordinates are still 0: a_j does not depend on them
     }
-    c[j] = neg ? p.L[j] - 1 - tj : tj;
+    const int cj = neg ? ext - 1 - tj : tj;
+    c[j] = j == 1 ? cj * p.CT : cj;
     base += c[j] * p.lstride[j];
   }
   double b0;
@@ -158,7 +165,7 @@ __device__ __forceinline__ int pencil_decode(const CellParams &p, int u, int (&c
   return base;
 }
 
-// Unit index (pencil mode) of the pencil holding a cell with coordinates c.
+// Unit index (pencil mode) of the unit holding a cell with coordinates c.
 template <int D>
 __device__ __forceinline__ int unit_of(const CellParams &p, const int (&c)[kMaxD]) {
   int cc[kMaxD], u = 0;
@@ -172,7 +179,9 @@ __device__ __forceinline__ int unit_of(const CellParams &p, const int (&c)[kMaxD
       cell_speed<D>(p, j, cc, b, neg);
     }
     cc[j] = c[j];
-    u += (neg ? p.L[j] - 1 - c[j] : c[j]) * p.ustride[j];
+    const int ext = j == 1 ? p.L[1] / p.CT : p.L[j];
+    const int cj = j == 1 ? c[1] / p.CT : c[j];
+    u += (neg ? ext - 1 - cj : cj) * p.ustride[j];
   }
   return u;
 }
@@ -213,7 +222,9 @@ __device__ __forceinline__ void decode_unit(const CellParams &p, int u, int j, U
     int cn[kMaxD];
 #pragma unroll
     for (int q = 0; q < kMaxD; ++q) cn[q] = c[q];
-    cn[j] = c[j] + (sg ? 1 : -1);
+    // the unit's boundary cell along dim 1 (its upwind end) reaches into the neighbouring block
+    if (j == 1) cn[1] = sg ? c[1] + p.CT - 1 : c[1];
+    cn[j] = cn[j] + (sg ? 1 : -1);
     int pu = -1, pd = 0, ps = 0;
     if (cn[j] >= 0 && cn[j] < p.L[j]) {
       pu = unit_of<D>(p, cn);
@@ -237,8 +248,9 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
 #pragma unroll
     for (int j = 0; j < kMaxD; ++j) c[j] = ui.c[j];
     const int g = step_group(p, gi, ui.dir0, ui.skew);
-    c[0] = g * p.CT + k;
-    first = ui.base + g * p.CT;
+    c[0] = g;
+    c[1] += k;
+    first = ui.base + g;
   } else {
     first = u * p.CT;
     int rr = first + k;
@@ -256,7 +268,7 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
   if (i == 0) {
     ci.cell = cell;
     ci.unit = u;
-    ci.cu = p.pencil ? c[0] : k;
+    ci.cu = p.pencil ? k * p.L[0] + c[0] : k;
   }
   double base;
   int sg;
@@ -272,14 +284,15 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
   unsigned char src = kSrcDirect, out = kOutNone;
   int nb = nbcell, slot = 0;
   if (i == 0 && p.pencil) {
-    // downwind-end cell of a group that has a successor in this unit feeds the carry
-    const int kd = k - up;
-    if ((kd < 0 || kd >= p.CT) && gi < p.GPU - 1) out = kOutCarry;
+    // every cell of a group feeds the carry of its pencil's next step
+    if (gi < p.GPU - 1) out = kOutCarry;
   }
   if (i > 0 && p.pub[i]) {
-    // downwind neighbour inside the local box: publish (its consumer runs a few groups later)
+    // downwind neighbour inside the local box and outside this group: publish (its consumer runs a
+    // few steps later)
     const int cd = c[i] - up;
-    if (cd >= 0 && cd < p.L[i]) out = kOutPub;
+    const bool in_group = p.pencil && i == 1 && k - up >= 0 && k - up < p.CT;
+    if (cd >= 0 && cd < p.L[i] && !in_group) out = kOutPub;
   }
   if (outside && p.xsplit[i]) {
     // the upwind neighbour lives on another rank: its trace arrived in the halo buffer
@@ -290,15 +303,12 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
     if (!p.pencil) {
       src = kSrcGroup;
       nb = k + (cn - c[0]);
-    } else {
-      const int kk = k + up;
-      if (kk >= 0 && kk < p.CT) {
-        src = kSrcGroup;
-        nb = kk;
-      } else if (gi > 0) {
-        src = kSrcCarry;
-      }
+    } else if (gi > 0) {
+      src = kSrcCarry;  // the previous step processed the upwind neighbour along dim 0
     }
+  } else if (p.pencil && i == 1 && k + up >= 0 && k + up < p.CT) {
+    src = kSrcGroup;  // the neighbour pencil is in this group
+    nb = k + up;
   } else if (!p.pencil && nbcell >= first && nbcell < first + p.CT) {
     src = kSrcGroup;
     nb = nbcell - first;
@@ -306,16 +316,21 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
     // the producer finished the step that processed the neighbour's group (the flag counts the steps
     // completed in this launch)?
     const int pu = ui.pu[i];
-    const int need = p.epoch | (group_step(p, c[0] / p.CT, ui.pdir0[i], ui.pskew[i]) + 1);
+    const int need = p.epoch | (group_step(p, c[0], ui.pdir0[i], ui.pskew[i]) + 1);
     if (ld_acquire(p.flags + pu) >= need) {
       src = kSrcPub;
-      slot = pu;
+      // the neighbour's slot in the producer unit: same (pencil, c_0), except along dim 1 where the
+      // neighbour is the other end of the neighbouring block
+      const int kn = (p.pencil && i == 1) ? (k + up + p.CT) % p.CT : k;
+      slot = pu * p.UC + (p.pencil ? kn * p.L[0] + c[0] : kn);
     }
   }
   ci.src[i] = src;
   ci.out[i] = out;
   ci.nb[i] = nb;
   ci.slot[i] = slot;
+  ci.tsrc[i] = src == kSrcPub ? p.tbuf[i] + (size_t)slot * p.FN
+               : src == kSrcHalo ? p.hbuf[i] + (size_t)slot * p.FN : nullptr;
 }
 
 // Cell-local offset (dim-X digit 0) of face point f = N r + l of dim X in the phase layout of X: rest
@@ -481,36 +496,38 @@ __device__ __forceinline__ void load_vec(const double *src, double (&t)[N], bool
   }
 }
 
-// pointer to this thread's N values of the published / halo trace of dim X
+// Early part of the upwind trace of dim X: the sources that are a plain N-value smem load (carry, and
+// the published / halo traces the CTA staged in TR). In-group (smem) and direct (global) traces are
+// contracted after the passes.
 template <int D, int N>
-__device__ __forceinline__ const double *remote_trace(const CellParams &p, const CellInfo &ci, int X, int r) {
-  using G = CGeo<D, N>;
-  if (ci.src[X] == kSrcPub) return p.tbuf[X] + ((size_t)ci.slot[X] * p.UC + ci.cu) * G::FN + (size_t)N * r;
-  return p.hbuf[X] + (size_t)ci.slot[X] * G::FN + (size_t)N * r;
-}
-
-// Early part of the upwind trace of dim X: the sources that are a plain N-value load (carry, published,
-// halo). In-group (smem) and direct (global) traces are contracted after the passes.
-template <int D, int N, int SX, int SY>
-__device__ __forceinline__ void trace_early(const CellParams &p, const CellInfo &ci, int X, int sR, int r,
-                                            const double *Ugroup, const double *carry_in, double (&t)[N]) {
+__device__ __forceinline__ void trace_early(const CellInfo &ci, int X, int r, const double *carry_in,
+                                            const double *TRx, double (&t)[N]) {
   switch (ci.src[X]) {
     case kSrcCarry:
       load_vec<N>(carry_in + N * r, t, false);
       break;
     case kSrcPub:
     case kSrcHalo:
-      load_vec<N>(remote_trace<D, N>(p, ci, X, r), t, true);
+      load_vec<N>(TRx + N * r, t, false);
       break;
     default:
       break;
   }
 }
 
+// Smem pointers of one group: its cells (U), their dU (RK), the running accumulator, the staged traces
+// of every phase ([phase][cell][P|Q][n^(d-1)]) and the dim-0 carry.
+struct GroupBufs {
+  const double *U, *DU;
+  double *ACC;
+  const double *TR;
+  const double *carry_in;
+  double *carry_out;
+};
+
 template <int D, int N, int MODE, int PH>
 __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
-                                          const double *Ug, double *ACC, const double *carry_in, double *carry_out,
-                                          bool active) {
+                                          const GroupBufs &gb, bool active) {
   if (!active) return;  // padding threads of the CTA: only the barriers between phases
   using G = CGeo<D, N>;
   constexpr int P = G::P(PH), Q = G::Q(PH);
@@ -523,8 +540,9 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   thread_phase<D, N, PH, LAST && MODE == kModeAdvection>(p, r, stab, stab + 8, tp);
   const int R = tp.R;
   const int sR = swz<D, N>(R);
-  const double *U = Ug + (size_t)k * G::ND;
-  double *A = ACC + (size_t)k * G::ND;
+  const double *U = gb.U + (size_t)k * G::ND;
+  double *A = gb.ACC + (size_t)k * G::ND;
+  const double *TRk = gb.TR + ((size_t)PH * p.CT + k) * 2 * G::FN;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
   const size_t g0 = (size_t)ci.cell * G::ND + R;
   // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line (a_i varies only with the other dims)
@@ -532,11 +550,10 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   const double s0P = (ci.base[P] + tp.wP) * facP, slP = p.a_lin[P][Q] * p.h[Q] * facP;
   const double s0Q = (ci.base[Q] + tp.wQ) * facQ, slQ = p.a_lin[Q][P] * p.h[P] * facQ;
 
-  // upwind traces from smem / the published and halo buffers, issued before the passes (their L2
-  // latency hides behind the passes; the carry may then be overwritten in place by this pass)
+  // upwind traces staged in smem, read before the passes (the carry may then be overwritten in place)
   double tP[N], tQ[N];
-  trace_early<D, N, SP, SQ>(p, ci, P, sR, r, Ug, carry_in, tP);
-  if constexpr (QA) trace_early<D, N, SQ, SP>(p, ci, Q, sR, r, Ug, carry_in, tQ);
+  trace_early<D, N>(ci, P, r, gb.carry_in, TRk, tP);
+  if constexpr (QA) trace_early<D, N>(ci, Q, r, gb.carry_in, TRk + G::FN, tQ);
 
   double acc[N][N];
   {
@@ -562,18 +579,6 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
         for (int b = 0; b < N; ++b) acc[a][b] = A[sidx<D, N>(sR, a * SP + b * SQ)];
     }
-    if constexpr (LAST && MODE == kModeRK) {
-      const unsigned long long pol = evict_first_policy();
-      // dU of the tile -> this thread's own ACC positions (already consumed), asynchronously; read back
-      // in the epilogue, so its HBM latency overlaps the passes and the lifts
-#pragma unroll
-      for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int b = 0; b < N; ++b)
-          if constexpr (HD_DU_HINT) cp_async8_ef(A + sidx<D, N>(sR, a * SP + b * SQ), p.du + g0 + a * SP + b * SQ, pol);
-          else cp_async8(A + sidx<D, N>(sR, a * SP + b * SQ), p.du + g0 + a * SP + b * SQ);
-      cp_async_commit();
-    }
     // volume terms of P and Q and this cell's downwind traces along P and Q
     double trP[N], trQ[N];
     const unsigned char oP = ci.out[P], oQ = QA ? ci.out[Q] : (unsigned char)kOutNone;
@@ -594,7 +599,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       }
     }
     // publish the downwind traces (dim 0 only ever feeds the carry; it is always P of phase 0)
-    if (oP == kOutCarry) store_vec<N>(carry_out + N * r, trP, false);
+    if (oP == kOutCarry) store_vec<N>(gb.carry_out + N * r, trP, false);
     else if (oP == kOutPub) store_vec<N>(p.tbuf[P] + ((size_t)ci.unit * p.UC + ci.cu) * G::FN + (size_t)N * r, trP, true);
     if constexpr (QA) {
       if (oQ == kOutPub)
@@ -603,10 +608,10 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   }
 
   // in-group neighbours (smem) and direct reads of the upwind neighbour (traces not published in time)
-  if (ci.src[P] == kSrcGroup) trace_smem<D, N, SP, SQ>(Ug + (size_t)ci.nb[P] * G::ND, sR, sgP, tP);
+  if (ci.src[P] == kSrcGroup) trace_smem<D, N, SP, SQ>(gb.U + (size_t)ci.nb[P] * G::ND, sR, sgP, tP);
   else if (ci.src[P] == kSrcDirect) trace_global<D, N, SP, SQ>(p.u + (size_t)ci.nb[P] * G::ND + R, sgP, tP);
   if constexpr (QA) {
-    if (ci.src[Q] == kSrcGroup) trace_smem<D, N, SQ, SP>(Ug + (size_t)ci.nb[Q] * G::ND, sR, sgQ, tQ);
+    if (ci.src[Q] == kSrcGroup) trace_smem<D, N, SQ, SP>(gb.U + (size_t)ci.nb[Q] * G::ND, sR, sgQ, tQ);
     else if (ci.src[Q] == kSrcDirect) trace_global<D, N, SQ, SP>(p.u + (size_t)ci.nb[Q] * G::ND + R, sgQ, tQ);
   }
 
@@ -643,22 +648,6 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       }
     }
   }
-  // published traces are consumed exactly once: drop their L2 lines without write-back (one lane per
-  // 128-byte line, after the whole warp has its values)
-  if constexpr ((N * 8) <= 128 && 128 % (N * 8) == 0) {
-    constexpr int TPL = 128 / (N * 8);  // threads per line
-    if (p.discard && p.pubany) {
-      // lanes of this warp that run the phase (padding threads k >= CT returned at the top)
-      const int wb = (int)(threadIdx.x & ~31u), nact = p.CT * G::NT - wb;
-      __syncwarp(nact >= 32 ? 0xffffffffu : ((1u << nact) - 1u));
-    }
-    if (p.discard && p.pubany && r % TPL == 0) {
-      if (ci.src[P] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, P, r));
-      if constexpr (QA) {
-        if (ci.src[Q] == kSrcPub) discard_l2_line(remote_trace<D, N>(p, ci, Q, r));
-      }
-    }
-  }
 
   if constexpr (!LAST) {
 #pragma unroll
@@ -673,61 +662,49 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int b = 0; b < N; ++b) __stcs(p.out + g0 + a * SP + b * SQ, acc[a][b] * (wr * (T.w[a] * T.w[b])));
   } else {
-    // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU
-    if constexpr (MODE == kModeRK) cp_async_wait<0>();
+    // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU (dU staged with the cells)
+    const double *DUk = gb.DU + (size_t)k * G::ND;
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         const int o = sidx<D, N>(sR, a * SP + b * SQ);
         double dun = acc[a][b];
-        if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
+        if constexpr (MODE == kModeRK) dun = fma(p.rk_a, DUk[o], dun);
         __stcs(p.du + g0 + a * SP + b * SQ, dun);
         __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, dun, U[o]));
       }
   }
 }
 
-// One group (all phases). Not inlined into the persistent loop, so that group-invariant values are not
-// hoisted out of it and kept live in registers across the whole loop.
-template <int D, int N, int MODE>
-__device__ HD_PG_INLINE void process_group(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
-                                           const double *Ug, double *ACC, const double *carry_in, double *carry_out,
-                                           bool active) {
-  using G = CGeo<D, N>;
-  run_phase<D, N, MODE, 0>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
-  if constexpr (G::NPH > 1) {
-    __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
-  }
-  if constexpr (G::NPH > 2) {
-    __syncthreads();
-    run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, Ug, ACC, carry_in, carry_out, active);
-  }
-}
-
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * G::ND + (CT > 1 ? 2 : 1) * G::FN + 16) * 8 + CT * (int)sizeof(CellInfo) +
-         2 * (int)sizeof(UnitInfo);
+  return (5 * CT * G::ND + G::NPH * CT * 2 * G::FN + CT * G::FN + 16) * 8 +
+         2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo);
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
+// Software pipeline: while group g is computed, the cells and dU of group g+1 stream in
+// (cp.async, double buffers), group g+1 is decoded and its producers' flags checked during g's
+// next-to-last phase, and its published/halo traces are staged in smem during g's last phase (those of
+// the last phase at the start of g+1) -- so the phases themselves only touch smem, except for the
+// direct-read fallback and the streaming stores.
 template <int D, int N, int MODE>
 __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constant__ CellParams p) {
   using G = CGeo<D, N>;
+  constexpr int NPH = G::NPH;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
+  const int CND = CT * G::ND;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  double *ACC = smem + 2 * CT * G::ND;  // U double buffer: smem + (it & 1) * CT * ND
-  // carry of the dim-0 trace between consecutive groups: one buffer when CT == 1 (the same thread reads
-  // it before overwriting it), two alternating buffers otherwise
-  const int ncarry = CT > 1 ? 2 : 1;
-  double *carry0 = ACC + CT * G::ND;
-  double *stab = carry0 + ncarry * G::FN;                    // xi[8], w[8]
-  CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);  // CT entries
-  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info + CT);  // 2 entries
+  // U[2] | DU[2] | ACC | TR[NPH][CT][2][FN] | carry | stab | info[2][CT] | uinfo[2]
+  double *ACC = smem + 4 * CND;
+  double *TR = ACC + CND;
+  double *carry0 = TR + NPH * CT * 2 * G::FN;                // [CT][FN]: per pencil, read before written
+  double *stab = carry0 + CT * G::FN;                        // xi[8], w[8]
+  CellInfo *info0 = reinterpret_cast<CellInfo *>(stab + 16);  // [2][CT]
+  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info0 + 2 * CT);
   const int tid = threadIdx.x;
   const int k = tid / G::NT;
   const int r = tid - k * G::NT;
@@ -738,66 +715,151 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   }
   if ((int)blockIdx.x >= p.nunits) return;
 
-  auto copy_group = [&](int first_cell, double *dst) {
-    const double *src = p.u + (size_t)first_cell * G::ND;
-    const int total = CT * G::ND;
+  // the group's cells: CT cells at cell stride cs (adjacent pencils in pencil mode, consecutive else)
+  const size_t cs = p.pencil ? (size_t)p.lstride[1] : 1;
+  auto copy_cells = [&](const double *base, int first_cell, double *dst) {
     if constexpr (G::ND % 2 == 0) {
-      for (int i = tid; i < (total >> 1); i += blockDim.x) {
+      for (int i = tid; i < (CND >> 1); i += blockDim.x) {
         const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
-        cp_async16(dst + kc * G::ND + swz<D, N>(x), src + e);
+        cp_async16(dst + kc * G::ND + swz<D, N>(x), base + ((size_t)first_cell + kc * cs) * G::ND + x);
       }
     } else {
-      for (int i = tid; i < total; i += blockDim.x) cp_async8(dst + i, src + i);
+      for (int i = tid; i < CND; i += blockDim.x) {
+        const int kc = i / G::ND, x = i - kc * G::ND;
+        cp_async8(dst + i, base + ((size_t)first_cell + kc * cs) * G::ND + x);
+      }
     }
   };
+  // stage (or discard the L2 lines of) the published / halo traces phase ph of a group needs; the work
+  // items (cell, P|Q, 16-byte chunk) are spread over all threads, the source pointers were prepared by
+  // the decode (CellInfo::tsrc)
+  auto stage_traces = [&](int ph, const CellInfo *inf, bool discard) {
+    const int P = G::P(ph), Q = G::Q(ph);
+    const int nslot = (ph == 0 || 2 * ph != D - 1) ? 2 : 1;
+    if (discard) {
+      if (!p.discard || (G::FN * 8) % 128 != 0) return;
+      constexpr int NL = G::FN * 8 / 128;  // 128-byte lines per trace
+      for (int i = tid; i < CT * nslot * NL; i += blockDim.x) {
+        const int e = i / NL, l = i - e * NL;
+        const int kk = e / nslot, X = (e - kk * nslot) ? Q : P;
+        if (inf[kk].src[X] == kSrcPub) discard_l2_line(inf[kk].tsrc[X] + l * 16);
+      }
+      return;
+    }
+    constexpr int CH = (G::FN % 2 == 0) ? 2 : 1;  // doubles per copy
+    constexpr int NCH = G::FN / CH;
+    for (int i = tid; i < CT * nslot * NCH; i += blockDim.x) {
+      const int e = i / NCH, ch = i - e * NCH;
+      const int kk = e / nslot, sl = e - kk * nslot;
+      const double *g = inf[kk].tsrc[sl ? Q : P];
+      if (!g) continue;
+      double *d = TR + ((size_t)(ph * CT + kk) * 2 + sl) * G::FN + ch * CH;
+      if constexpr (CH == 2) cp_async16(d, g + ch * CH);
+      else cp_async8(d, g + ch * CH);
+    }
+  };
+  auto first_cell = [&](int uu, int g, const UnitInfo &ui) {
+    return p.pencil ? ui.base + step_group(p, g, ui.dir0, ui.skew) : uu * CT;
+  };
+  auto decode_group = [&](int uu, int g, const UnitInfo &ui, CellInfo *inf) {
+    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
+      const int kk = idx / D;
+      decode_cell<D>(p, ui, uu, g, kk, inf[kk], idx - kk * D);
+    }
+  };
+  const bool rk = MODE == kModeRK;
 
-  // unit-decode cache: slot (j & 1) holds this CTA's j-th unit; the next unit is decoded while the
-  // current one starts (its first group's cells are prefetched during the current unit's last group)
+  // prologue: decode unit(s) and group 0, stage its early traces, its cells and dU
   int u = blockIdx.x, gi = 0, it = 0, ju = 0;
   if (p.pencil) {
     if (tid < D) decode_unit<D>(p, u, tid, uinfo[0]);
-    if (tid >= 32 && tid < 32 + D && u + (int)gridDim.x < p.nunits)
-      decode_unit<D>(p, u + gridDim.x, tid - 32, uinfo[1]);
+    if (tid >= 32 && tid < 32 + D && u + (int)gridDim.x < p.nunits) decode_unit<D>(p, u + gridDim.x, tid - 32, uinfo[1]);
     __syncthreads();
   }
-  auto first_cell = [&](int uu, int g, const UnitInfo &ui) {
-    return p.pencil ? ui.base + step_group(p, g, ui.dir0, ui.skew) * CT : uu * CT;
-  };
-  copy_group(first_cell(u, 0, uinfo[0]), smem);
+  decode_group(u, 0, uinfo[0], info0);
+  __syncthreads();
+  for (int ph = 0; ph + 1 < NPH; ++ph) stage_traces(ph, info0, false);
   cp_async_commit();
+  {
+    const int f0 = first_cell(u, 0, uinfo[0]);
+    copy_cells(p.u, f0, smem);
+    if (rk) copy_cells(p.du, f0, smem + 2 * CND);
+  }
+  cp_async_commit();
+
   int prev_unit = -1, prev_step = 0;
   while (u < p.nunits) {
-    // next group (this unit or the first group of the next unit)
+    const int s = it & 1;
+    CellInfo *info = info0 + s * CT;
+    CellInfo *info_next = info0 + (s ^ 1) * CT;
     int un = u, gn = gi + 1;
     if (gn >= p.GPU) {
       un = u + gridDim.x;
       gn = 0;
     }
-    __syncthreads();  // previous group finished: info, carry and the other U buffer are free
-    if (prev_unit >= 0 && tid == 0) {
-      // the previous group's traces are all written (barrier above): publish its progress
-      __threadfence();
-      *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
-    }
+    const bool has_next = un < p.nunits;
+    const UnitInfo &ui_next = uinfo[(ju + (gn == 0 ? 1 : 0)) & 1];
+    __syncthreads();  // group g-1 done: ACC, carry, TR[last], U/DU[s^1], info[s^1] are free
     if (p.pencil && gi == 0 && ju > 0) {
       // decode the next unit into the slot the previous unit used
       const int u2 = u + gridDim.x;
       if (tid < D && u2 < p.nunits) decode_unit<D>(p, u2, tid, uinfo[(ju + 1) & 1]);
-      if (p.GPU == 1) __syncthreads();  // needed right below by the prefetch
+      if (p.GPU == 1) __syncthreads();  // needed right below by the prefetch and the decode
     }
-    if (un < p.nunits) copy_group(first_cell(un, gn, uinfo[(ju + (gn == 0 ? 1 : 0)) & 1]),
-                                  smem + ((it + 1) & 1) * CT * G::ND);
+    stage_traces(NPH - 1, info, false);  // this group's last-phase traces (B)
     cp_async_commit();
-    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
-      const int kk = idx / D;
-      decode_cell<D>(p, uinfo[ju & 1], u, gi, kk, info[kk], idx - kk * D);
+    if (has_next) {  // the next group's cells and dU (A)
+      const int f1 = first_cell(un, gn, ui_next);
+      copy_cells(p.u, f1, smem + (s ^ 1) * CND);
+      if (rk) copy_cells(p.du, f1, smem + (2 + (s ^ 1)) * CND);
     }
-    cp_async_wait<1>();
+    cp_async_commit();
+    cp_async_wait<2>();  // this group's cells, dU and early-phase traces
     __syncthreads();
-    // every thread enters (the phases are separated by CTA barriers); padding threads idle inside
-    process_group<D, N, MODE>(p, info[active ? k : 0], stab, k, r, smem + (it & 1) * CT * G::ND, ACC,
-                              carry0 + (ncarry > 1 ? ((gi + 1) & 1) : 0) * G::FN,
-                              carry0 + (ncarry > 1 ? (gi & 1) : 0) * G::FN, active);
+    for (int ph = 0; ph + 1 < NPH; ++ph) stage_traces(ph, info, true);
+    GroupBufs gb;
+    gb.U = smem + s * CND;
+    gb.DU = smem + (2 + s) * CND;
+    gb.ACC = ACC;
+    gb.TR = TR;
+    gb.carry_in = carry0 + (size_t)(active ? k : 0) * G::FN;
+    gb.carry_out = carry0 + (size_t)(active ? k : 0) * G::FN;
+    const CellInfo &ci = info[active ? k : 0];
+    // before the last phase: decode the next group (its producers are >= one step ahead), wait for the
+    // last-phase traces and the prefetch, then stage the next group's early-phase traces
+    auto before_last = [&]() {
+      if (has_next) decode_group(un, gn, ui_next, info_next);
+      cp_async_wait<0>();
+      __syncthreads();
+      stage_traces(NPH - 1, info, true);
+      if (has_next)
+        for (int ph = 0; ph + 1 < NPH; ++ph) stage_traces(ph, info_next, false);
+      cp_async_commit();
+    };
+    auto publish_prev = [&]() {
+      // progress of the previous group: its traces were written before the barriers above
+      if (prev_unit >= 0 && tid == (int)blockDim.x - 1) {
+        __threadfence();
+        *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
+      }
+    };
+    if constexpr (NPH == 1) {
+      before_last();
+      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+      publish_prev();
+    } else {
+      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+      publish_prev();
+      if constexpr (NPH == 2) {
+        before_last();
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+      } else {
+        __syncthreads();
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+        before_last();
+        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, gb, active);
+      }
+    }
     prev_unit = p.pubany ? u : -1;
     prev_step = gi;
     if (gn == 0) ++ju;
@@ -808,7 +870,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   cp_async_wait<0>();
   if (prev_unit >= 0) {
     __syncthreads();
-    if (tid == 0) {
+    if (tid == (int)blockDim.x - 1) {
       __threadfence();
       *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
     }

@@ -54,9 +54,9 @@ bool make_partition(const hd_mesh_desc &ds, Partition &pt, std::string &err);
 void make_halo(const hd_mesh_desc &ds, const Partition &pt, const double *h, int i, HaloDim &hd);
 
 // Kernel parameters of the fused cell kernel (passed by value as __grid_constant__).
-// Work decomposition: a group = CT cells consecutive along dim 0; a unit = the groups one
-// CTA processes back to back: a pencil of L_0 cells (pencil mode, CT | L_0) or a single group holding
-// whole pencils (L_0 | CT).
+// Work decomposition: pencil mode -- a group = CT cells at one dim-0 position from CT
+// adjacent pencils (CT | L_1), a unit = those CT pencils, one group per step; multi-pencil mode (small
+// d) -- a group = CT consecutive cells holding whole pencils, one group per unit.
 struct CellParams {
   const double *u;        // operator input (never written by the kernel)
   double *out;            // A-mode: v; RK-mode: U_new
@@ -68,8 +68,9 @@ struct CellParams {
   double jdet;            // |J| = prod h_i
   int nunits;             // units of this launch
   int CT;                 // cells per group
-  int GPU;                // groups per unit
+  int GPU;                // groups (steps) per unit
   int UC;                 // cells per unit (trace-buffer slot size)
+  int FN;                 // n^(d-1): doubles per trace
   int pencil;             // 1: pencil mode
   int pubany;             // some dim publishes traces (unit flags needed)
   int L[kMaxD];           // cells per dim (local box)
@@ -133,7 +134,7 @@ bool cell_kernel_supported(int d, int n);
 struct CellGeometry {
   int CT, pencil, GPU, threads, smem, phases;
 };
-CellGeometry cell_geometry(int d, int n, int L0, long long ncells);
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells);
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd

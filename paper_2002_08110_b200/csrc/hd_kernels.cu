@@ -202,14 +202,14 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 namespace {
 
 template <int D, int N>
-CellGeometry geometry_dn(int L0, long long ncells) {
+CellGeometry geometry_dn(int L0, int L1, long long ncells) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
   const int maxCT = 256 / G::NT;
   const int kSmemMax = HD_MINB > 1 ? 113 * 1024 : 227 * 1024;
   auto smem_of = [&](int c) { return cell_smem_bytes<D, N>(c); };
-  if (L0 <= maxCT) {
+  if (L0 <= maxCT && smem_of(L0) <= kSmemMax) {
     // multi-pencil groups: m whole pencils per group
     const long long npen = ncells / L0;
     int m = 1;
@@ -219,12 +219,13 @@ CellGeometry geometry_dn(int L0, long long ncells) {
     g.pencil = 0;
     g.GPU = 1;
   } else {
+    // pencil mode: a group is CT cells from CT adjacent pencils (CT | L1), one group per dim-0 position
     int CT = 1;
     for (int c = 1; c <= maxCT; ++c)
-      if (L0 % c == 0 && smem_of(c) <= kSmemMax) CT = c;
+      if (L1 % c == 0 && smem_of(c) <= kSmemMax) CT = c;
     g.CT = CT;
     g.pencil = 1;
-    g.GPU = L0 / CT;
+    g.GPU = L0;
   }
   g.threads = ((g.CT * G::NT + 31) / 32) * 32;
   g.smem = smem_of(g.CT);
@@ -245,7 +246,7 @@ cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
 
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
-  const CellGeometry g = geometry_dn<D, N>(p.L[0], (long long)p.nunits * p.UC);
+  const CellGeometry g = geometry_dn<D, N>(p.L[0], p.L[1], (long long)p.nunits * p.UC);
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
   cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
@@ -364,8 +365,8 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s
   HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0, long long ncells) {
-  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, ncells)
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells)
 }
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
   HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)

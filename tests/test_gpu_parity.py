@@ -66,7 +66,7 @@ def small_specs():
         d_v = d - d_x
         for k in range(1, 6):
             n = k + 1
-            if n ** d > 7776 or n ** (d - 2) > 1024:
+            if n ** d > 4096 or n ** (d - 2) > 256:
                 continue
             cells = [3, 2, 2, 3, 2, 2][:d] if n ** d <= 1296 else [2] * d
             lo = [0.0, 0.1, -0.5, -2.0, -1.0, -1.5][:d]

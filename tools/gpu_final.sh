@@ -1,0 +1,29 @@
+#!/bin/bash
+# Round measurement: bench lines (6D default, 5D), launch list of the bench command, DRAM traffic of the
+# dominant kernel (6D and 5D, few-pass metric capture) and one full ncu capture (5D RK stage).
+O=gpurun_out
+export PATH=/usr/local/cuda/bin:$PATH
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/smi.txt 2>&1
+timeout 900 python bench.py > $O/bench_6d.json 2> $O/bench_6d.err; echo "bench 6d rc=$?"
+timeout 600 python bench.py --config 5d > $O/bench_5d.json 2> $O/bench_5d.err; echo "bench 5d rc=$?"
+timeout 600 python bench.py --config 4d --no-cpu > $O/bench_4d.json 2> $O/bench_4d.err; echo "bench 4d rc=$?"
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref_6d.json 2> $O/bench_ref.err; echo "ref rc=$?"
+# launch list of the bench command (same command, fewer steps; cold-cache serialised times: shares only)
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $O/plain_bench.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_6d.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $O/ncu_launches.log 2>&1; echo "launches rc=$?"
+# DRAM traffic per launch of the fused stage kernel (RK mode, steady state)
+for c in 6d 5d; do
+  timeout 300 python tools/prof_driver.py --config $c --op rk --reps 2 > $O/plain_traffic_$c.log 2>&1 && \
+  timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct \
+    --clock-control none -k regex:cell_kernel -s 6 -c 2 --csv --log-file $O/traffic_$c.csv \
+    python tools/prof_driver.py --config $c --op rk --reps 2 > $O/ncu_traffic_$c.log 2>&1; echo "traffic $c rc=$?"
+done
+# one full capture of the dominant kernel (5D: the 6D replay has to save/restore 140 GB per pass)
+tag=full_5d
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:cell_kernel -s 6 -c 1 \
+   -o $O/ncu_$tag python tools/prof_driver.py --config 5d --op rk --reps 2 > $O/ncu_$tag.log 2>&1
+python tools/ncu_summary.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_$tag.txt 2>&1
+sz=$(stat -c %s $O/ncu_$tag.ncu-rep 2>/dev/null || echo 0)
+if [ "$sz" -gt 50000000 ]; then rm -f $O/ncu_$tag.ncu-rep; fi
+du -sh $O
