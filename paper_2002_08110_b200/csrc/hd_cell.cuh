@@ -496,31 +496,28 @@ __device__ __forceinline__ void load_vec(const double *src, double (&t)[N], bool
   }
 }
 
-// Early part of the upwind trace of dim X: the sources that are a plain N-value smem load (carry, and
-// the published / halo traces the CTA staged in TR). In-group (smem) and direct (global) traces are
-// contracted after the passes.
+// Early part of the upwind trace of dim X: the sources that are a plain N-value load -- the carry (smem)
+// and the published / halo traces (global, L2: issued before the passes so the latency hides behind
+// them). In-group (smem) and direct (global) traces are contracted after the passes.
 template <int D, int N>
-__device__ __forceinline__ void trace_early(const CellInfo &ci, int X, int r, const double *carry_in,
-                                            const double *TRx, double (&t)[N]) {
+__device__ __forceinline__ void trace_early(const CellInfo &ci, int X, int r, const double *carry_in, double (&t)[N]) {
   switch (ci.src[X]) {
     case kSrcCarry:
       load_vec<N>(carry_in + N * r, t, false);
       break;
     case kSrcPub:
     case kSrcHalo:
-      load_vec<N>(TRx + N * r, t, false);
+      load_vec<N>(ci.tsrc[X] + N * r, t, true);
       break;
     default:
       break;
   }
 }
 
-// Smem pointers of one group: its cells (U), their dU (RK), the running accumulator, the staged traces
-// of every phase ([phase][cell][P|Q][n^(d-1)]) and the dim-0 carry.
+// Smem pointers of one group: its cells (U), the running accumulator and the dim-0 carry.
 struct GroupBufs {
-  const double *U, *DU;
+  const double *U;
   double *ACC;
-  const double *TR;
   const double *carry_in;
   double *carry_out;
 };
@@ -542,7 +539,6 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   const int sR = swz<D, N>(R);
   const double *U = gb.U + (size_t)k * G::ND;
   double *A = gb.ACC + (size_t)k * G::ND;
-  const double *TRk = gb.TR + ((size_t)PH * p.CT + k) * 2 * G::FN;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
   const size_t g0 = (size_t)ci.cell * G::ND + R;
   // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line (a_i varies only with the other dims)
@@ -550,10 +546,10 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   const double s0P = (ci.base[P] + tp.wP) * facP, slP = p.a_lin[P][Q] * p.h[Q] * facP;
   const double s0Q = (ci.base[Q] + tp.wQ) * facQ, slQ = p.a_lin[Q][P] * p.h[P] * facQ;
 
-  // upwind traces staged in smem, read before the passes (the carry may then be overwritten in place)
+  // carry / published / halo traces, read before the passes (the carry may then be overwritten in place)
   double tP[N], tQ[N];
-  trace_early<D, N>(ci, P, r, gb.carry_in, TRk, tP);
-  if constexpr (QA) trace_early<D, N>(ci, Q, r, gb.carry_in, TRk + G::FN, tQ);
+  trace_early<D, N>(ci, P, r, gb.carry_in, tP);
+  if constexpr (QA) trace_early<D, N>(ci, Q, r, gb.carry_in, tQ);
 
   double acc[N][N];
   {
@@ -578,6 +574,15 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int b = 0; b < N; ++b) acc[a][b] = A[sidx<D, N>(sR, a * SP + b * SQ)];
+    }
+    if constexpr (LAST && MODE == kModeRK) {
+      // dU of the tile -> this thread's own ACC positions (already consumed), asynchronously; read back
+      // in the epilogue, so its HBM latency overlaps the passes and the lifts
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) cp_async8(A + sidx<D, N>(sR, a * SP + b * SQ), p.du + g0 + a * SP + b * SQ);
+      cp_async_commit();
     }
     // volume terms of P and Q and this cell's downwind traces along P and Q
     double trP[N], trQ[N];
@@ -649,6 +654,23 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     }
   }
 
+  // published traces are consumed exactly once: drop their L2 lines without write-back (one lane per
+  // 128-byte line, after the lanes sharing it have their values)
+  if constexpr ((N * 8) <= 128 && 128 % (N * 8) == 0) {
+    constexpr int TPL = 128 / (N * 8);  // threads per line
+    if (p.discard && p.pubany) {
+      // lanes of this warp that run the phase (padding threads k >= CT returned at the top)
+      const int wb = (int)(threadIdx.x & ~31u), nact = p.CT * G::NT - wb;
+      __syncwarp(nact >= 32 ? 0xffffffffu : ((1u << nact) - 1u));
+      if (r % TPL == 0) {
+        if (ci.src[P] == kSrcPub) discard_l2_line(ci.tsrc[P] + N * r);
+        if constexpr (QA) {
+          if (ci.src[Q] == kSrcPub) discard_l2_line(ci.tsrc[Q] + N * r);
+        }
+      }
+    }
+  }
+
   if constexpr (!LAST) {
 #pragma unroll
     for (int a = 0; a < N; ++a)
@@ -662,15 +684,15 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int b = 0; b < N; ++b) __stcs(p.out + g0 + a * SP + b * SQ, acc[a][b] * (wr * (T.w[a] * T.w[b])));
   } else {
-    // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU (dU staged with the cells)
-    const double *DUk = gb.DU + (size_t)k * G::ND;
+    // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU
+    if constexpr (MODE == kModeRK) cp_async_wait<0>();
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         const int o = sidx<D, N>(sR, a * SP + b * SQ);
         double dun = acc[a][b];
-        if constexpr (MODE == kModeRK) dun = fma(p.rk_a, DUk[o], dun);
+        if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
         __stcs(p.du + g0 + a * SP + b * SQ, dun);
         __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, dun, U[o]));
       }
@@ -680,31 +702,27 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (5 * CT * G::ND + G::NPH * CT * 2 * G::FN + CT * G::FN + 16) * 8 +
+  return (3 * CT * G::ND + CT * G::FN + 16) * 8 +
          2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo);
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
-// Software pipeline: while group g is computed, the cells and dU of group g+1 stream in
-// (cp.async, double buffers), group g+1 is decoded and its producers' flags checked during g's
-// next-to-last phase, and its published/halo traces are staged in smem during g's last phase (those of
-// the last phase at the start of g+1) -- so the phases themselves only touch smem, except for the
-// direct-read fallback and the streaming stores.
+// Per group: the next group's cells stream in (cp.async, double buffer) while this one is computed; the
+// group is decoded (incl. the producer-flag checks) after the previous one finished; the progress flag of
+// the previous group is released by the last thread, off the decode threads' path.
 template <int D, int N, int MODE>
 __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constant__ CellParams p) {
   using G = CGeo<D, N>;
-  constexpr int NPH = G::NPH;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
   const int CND = CT * G::ND;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  // U[2] | DU[2] | ACC | TR[NPH][CT][2][FN] | carry | stab | info[2][CT] | uinfo[2]
-  double *ACC = smem + 4 * CND;
-  double *TR = ACC + CND;
-  double *carry0 = TR + NPH * CT * 2 * G::FN;                // [CT][FN]: per pencil, read before written
-  double *stab = carry0 + CT * G::FN;                        // xi[8], w[8]
-  CellInfo *info0 = reinterpret_cast<CellInfo *>(stab + 16);  // [2][CT]
-  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info0 + 2 * CT);
+  // U[2] | ACC | carry[CT][FN] | stab | info[CT] | uinfo[2]
+  double *ACC = smem + 2 * CND;
+  double *carry0 = ACC + CND;                                 // per pencil, read before written
+  double *stab = carry0 + CT * G::FN;                         // xi[8], w[8]
+  CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);   // [CT]
+  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info + CT);  // [2]
   const int tid = threadIdx.x;
   const int k = tid / G::NT;
   const int r = tid - k * G::NT;
@@ -717,148 +735,72 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
 
   // the group's cells: CT cells at cell stride cs (adjacent pencils in pencil mode, consecutive else)
   const size_t cs = p.pencil ? (size_t)p.lstride[1] : 1;
-  auto copy_cells = [&](const double *base, int first_cell, double *dst) {
+  auto copy_cells = [&](int first_cell, double *dst) {
     if constexpr (G::ND % 2 == 0) {
       for (int i = tid; i < (CND >> 1); i += blockDim.x) {
         const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
-        cp_async16(dst + kc * G::ND + swz<D, N>(x), base + ((size_t)first_cell + kc * cs) * G::ND + x);
+        cp_async16(dst + kc * G::ND + swz<D, N>(x), p.u + ((size_t)first_cell + kc * cs) * G::ND + x);
       }
     } else {
       for (int i = tid; i < CND; i += blockDim.x) {
         const int kc = i / G::ND, x = i - kc * G::ND;
-        cp_async8(dst + i, base + ((size_t)first_cell + kc * cs) * G::ND + x);
+        cp_async8(dst + i, p.u + ((size_t)first_cell + kc * cs) * G::ND + x);
       }
-    }
-  };
-  // stage (or discard the L2 lines of) the published / halo traces phase ph of a group needs; the work
-  // items (cell, P|Q, 16-byte chunk) are spread over all threads, the source pointers were prepared by
-  // the decode (CellInfo::tsrc)
-  auto stage_traces = [&](int ph, const CellInfo *inf, bool discard) {
-    const int P = G::P(ph), Q = G::Q(ph);
-    const int nslot = (ph == 0 || 2 * ph != D - 1) ? 2 : 1;
-    if (discard) {
-      if (!p.discard || (G::FN * 8) % 128 != 0) return;
-      constexpr int NL = G::FN * 8 / 128;  // 128-byte lines per trace
-      for (int i = tid; i < CT * nslot * NL; i += blockDim.x) {
-        const int e = i / NL, l = i - e * NL;
-        const int kk = e / nslot, X = (e - kk * nslot) ? Q : P;
-        if (inf[kk].src[X] == kSrcPub) discard_l2_line(inf[kk].tsrc[X] + l * 16);
-      }
-      return;
-    }
-    constexpr int CH = (G::FN % 2 == 0) ? 2 : 1;  // doubles per copy
-    constexpr int NCH = G::FN / CH;
-    for (int i = tid; i < CT * nslot * NCH; i += blockDim.x) {
-      const int e = i / NCH, ch = i - e * NCH;
-      const int kk = e / nslot, sl = e - kk * nslot;
-      const double *g = inf[kk].tsrc[sl ? Q : P];
-      if (!g) continue;
-      double *d = TR + ((size_t)(ph * CT + kk) * 2 + sl) * G::FN + ch * CH;
-      if constexpr (CH == 2) cp_async16(d, g + ch * CH);
-      else cp_async8(d, g + ch * CH);
     }
   };
   auto first_cell = [&](int uu, int g, const UnitInfo &ui) {
     return p.pencil ? ui.base + step_group(p, g, ui.dir0, ui.skew) : uu * CT;
   };
-  auto decode_group = [&](int uu, int g, const UnitInfo &ui, CellInfo *inf) {
-    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
-      const int kk = idx / D;
-      decode_cell<D>(p, ui, uu, g, kk, inf[kk], idx - kk * D);
-    }
-  };
-  const bool rk = MODE == kModeRK;
 
-  // prologue: decode unit(s) and group 0, stage its early traces, its cells and dU
   int u = blockIdx.x, gi = 0, it = 0, ju = 0;
   if (p.pencil) {
     if (tid < D) decode_unit<D>(p, u, tid, uinfo[0]);
     if (tid >= 32 && tid < 32 + D && u + (int)gridDim.x < p.nunits) decode_unit<D>(p, u + gridDim.x, tid - 32, uinfo[1]);
     __syncthreads();
   }
-  decode_group(u, 0, uinfo[0], info0);
-  __syncthreads();
-  for (int ph = 0; ph + 1 < NPH; ++ph) stage_traces(ph, info0, false);
+  copy_cells(first_cell(u, 0, uinfo[0]), smem);
   cp_async_commit();
-  {
-    const int f0 = first_cell(u, 0, uinfo[0]);
-    copy_cells(p.u, f0, smem);
-    if (rk) copy_cells(p.du, f0, smem + 2 * CND);
-  }
-  cp_async_commit();
-
   int prev_unit = -1, prev_step = 0;
   while (u < p.nunits) {
-    const int s = it & 1;
-    CellInfo *info = info0 + s * CT;
-    CellInfo *info_next = info0 + (s ^ 1) * CT;
     int un = u, gn = gi + 1;
     if (gn >= p.GPU) {
       un = u + gridDim.x;
       gn = 0;
     }
-    const bool has_next = un < p.nunits;
-    const UnitInfo &ui_next = uinfo[(ju + (gn == 0 ? 1 : 0)) & 1];
-    __syncthreads();  // group g-1 done: ACC, carry, TR[last], U/DU[s^1], info[s^1] are free
+    __syncthreads();  // previous group finished: info, carry, ACC and the other U buffer are free
+    if (prev_unit >= 0 && tid == (int)blockDim.x - 1) {
+      // the previous group's traces are all written (barrier above): publish its progress
+      __threadfence();
+      *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
+    }
     if (p.pencil && gi == 0 && ju > 0) {
       // decode the next unit into the slot the previous unit used
       const int u2 = u + gridDim.x;
       if (tid < D && u2 < p.nunits) decode_unit<D>(p, u2, tid, uinfo[(ju + 1) & 1]);
-      if (p.GPU == 1) __syncthreads();  // needed right below by the prefetch and the decode
+      if (p.GPU == 1) __syncthreads();  // needed right below by the prefetch
     }
-    stage_traces(NPH - 1, info, false);  // this group's last-phase traces (B)
+    if (un < p.nunits) copy_cells(first_cell(un, gn, uinfo[(ju + (gn == 0 ? 1 : 0)) & 1]), smem + ((it + 1) & 1) * CND);
     cp_async_commit();
-    if (has_next) {  // the next group's cells and dU (A)
-      const int f1 = first_cell(un, gn, ui_next);
-      copy_cells(p.u, f1, smem + (s ^ 1) * CND);
-      if (rk) copy_cells(p.du, f1, smem + (2 + (s ^ 1)) * CND);
+    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
+      const int kk = idx / D;
+      decode_cell<D>(p, uinfo[ju & 1], u, gi, kk, info[kk], idx - kk * D);
     }
-    cp_async_commit();
-    cp_async_wait<2>();  // this group's cells, dU and early-phase traces
+    cp_async_wait<1>();
     __syncthreads();
-    for (int ph = 0; ph + 1 < NPH; ++ph) stage_traces(ph, info, true);
     GroupBufs gb;
-    gb.U = smem + s * CND;
-    gb.DU = smem + (2 + s) * CND;
+    gb.U = smem + (it & 1) * CND;
     gb.ACC = ACC;
-    gb.TR = TR;
     gb.carry_in = carry0 + (size_t)(active ? k : 0) * G::FN;
     gb.carry_out = carry0 + (size_t)(active ? k : 0) * G::FN;
     const CellInfo &ci = info[active ? k : 0];
-    // before the last phase: decode the next group (its producers are >= one step ahead), wait for the
-    // last-phase traces and the prefetch, then stage the next group's early-phase traces
-    auto before_last = [&]() {
-      if (has_next) decode_group(un, gn, ui_next, info_next);
-      cp_async_wait<0>();
+    run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+    if constexpr (G::NPH > 1) {
       __syncthreads();
-      stage_traces(NPH - 1, info, true);
-      if (has_next)
-        for (int ph = 0; ph + 1 < NPH; ++ph) stage_traces(ph, info_next, false);
-      cp_async_commit();
-    };
-    auto publish_prev = [&]() {
-      // progress of the previous group: its traces were written before the barriers above
-      if (prev_unit >= 0 && tid == (int)blockDim.x - 1) {
-        __threadfence();
-        *(volatile int *)(p.flags + prev_unit) = p.epoch | (prev_step + 1);
-      }
-    };
-    if constexpr (NPH == 1) {
-      before_last();
-      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
-      publish_prev();
-    } else {
-      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
-      publish_prev();
-      if constexpr (NPH == 2) {
-        before_last();
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
-      } else {
-        __syncthreads();
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
-        before_last();
-        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, gb, active);
-      }
+      run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+    }
+    if constexpr (G::NPH > 2) {
+      __syncthreads();
+      run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, gb, active);
     }
     prev_unit = p.pubany ? u : -1;
     prev_step = gi;
