@@ -81,7 +81,9 @@ struct CellInfo {
   int unit;                  // the unit being processed (kOutPub slot)
   int nb[kMaxD];             // kSrcDirect: neighbour cell index; kSrcGroup: neighbour slot k' in the group
   int slot[kMaxD];           // kSrcPub: producer trace index (unit * UC + cell slot); kSrcHalo: receive slot
-  const double *tsrc[kMaxD]; // kSrcPub / kSrcHalo: the trace to stage in smem (else null)
+  const double *tsrc[kMaxD]; // kSrcPub / kSrcHalo: the trace to read (else null)
+  int pflag[kMaxD];          // pending publication check: producer unit (-1: none)
+  int need[kMaxD];           // ... and the flag value that means "the neighbour's step is done"
   unsigned char src[kMaxD];  // TraceSrc of the upwind trace per dim
   unsigned char out[kMaxD];  // TraceOut of the downwind trace per dim
   unsigned char sg[kMaxD];   // 1: a_i < 0 on this cell (upwind neighbour at +e_i)
@@ -282,7 +284,7 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
   if (cn >= p.L[i]) cn -= p.L[i];
   const int nbcell = cell + (cn - c[i]) * p.lstride[i];
   unsigned char src = kSrcDirect, out = kOutNone;
-  int nb = nbcell, slot = 0;
+  int nb = nbcell, slot = 0, pflag = -1, need = 0;
   if (i == 0 && p.pencil) {
     // every cell of a group feeds the carry of its pencil's next step
     if (gi < p.GPU - 1) out = kOutCarry;
@@ -315,22 +317,31 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
   } else if (p.pub[i] && !outside && ui.pu[i] >= 0) {
     // the producer finished the step that processed the neighbour's group (the flag counts the steps
     // completed in this launch)?
-    const int pu = ui.pu[i];
-    const int need = p.epoch | (group_step(p, c[0], ui.pdir0[i], ui.pskew[i]) + 1);
-    if (ld_acquire(p.flags + pu) >= need) {
-      src = kSrcPub;
-      // the neighbour's slot in the producer unit: same (pencil, c_0), except along dim 1 where the
-      // neighbour is the other end of the neighbouring block
-      const int kn = (p.pencil && i == 1) ? (k + up + p.CT) % p.CT : k;
-      slot = pu * p.UC + (p.pencil ? kn * p.L[0] + c[0] : kn);
-    }
+    // publication check left pending (resolve_cell): the producer unit, the flag value meaning "the
+    // step that processed the neighbour's group is done", and the neighbour's slot in the producer
+    // unit (same pencil and c_0, except along dim 1 where it is the other end of the neighbouring block)
+    pflag = ui.pu[i];
+    need = p.epoch | (group_step(p, c[0], ui.pdir0[i], ui.pskew[i]) + 1);
+    const int kn = (p.pencil && i == 1) ? (k + up + p.CT) % p.CT : k;
+    slot = pflag * p.UC + (p.pencil ? kn * p.L[0] + c[0] : kn);
   }
   ci.src[i] = src;
   ci.out[i] = out;
   ci.nb[i] = nb;
   ci.slot[i] = slot;
-  ci.tsrc[i] = src == kSrcPub ? p.tbuf[i] + (size_t)slot * p.FN
-               : src == kSrcHalo ? p.hbuf[i] + (size_t)slot * p.FN : nullptr;
+  ci.pflag[i] = pflag;
+  ci.need[i] = need;
+  ci.tsrc[i] = src == kSrcHalo ? p.hbuf[i] + (size_t)slot * p.FN : nullptr;
+}
+
+// Resolve a pending publication check with the producer's flag value fv (fetched asynchronously).
+// Flags only grow within a launch (and a flag of an older launch is smaller), so a stale value can only
+// make the check fail, which falls back to a direct read.
+__device__ __forceinline__ void resolve_cell(const CellParams &p, CellInfo &ci, int i, int fv) {
+  if (ci.pflag[i] >= 0 && fv >= ci.need[i]) {
+    ci.src[i] = kSrcPub;
+    ci.tsrc[i] = p.tbuf[i] + (size_t)ci.slot[i] * p.FN;
+  }
 }
 
 // Cell-local offset (dim-X digit 0) of face point f = N r + l of dim X in the phase layout of X: rest
@@ -702,27 +713,31 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * G::ND + CT * G::FN + 16) * 8 +
-         2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo);
+  return (3 * CT * G::ND + CT * G::FN + 16) * 8 + 2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo) +
+         CT * D * 16 + 16;
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
-// Per group: the next group's cells stream in (cp.async, double buffer) while this one is computed; the
-// group is decoded (incl. the producer-flag checks) after the previous one finished; the progress flag of
-// the previous group is released by the last thread, off the decode threads' path.
+// Per group g: the cells of g+1 stream in (cp.async, double buffer) from g's start; g+1 is decoded at the
+// start of g's last phase, its producers' flags are fetched with 16-byte cp.async (completing with g's
+// epilogue) and checked after it -- so a group starts right after one barrier. The progress flag of a
+// group is released by the CTA's last thread at the next group's start.
 template <int D, int N, int MODE>
 __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constant__ CellParams p) {
   using G = CGeo<D, N>;
+  constexpr int NPH = G::NPH;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
   const int CND = CT * G::ND;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  // U[2] | ACC | carry[CT][FN] | stab | info[CT] | uinfo[2]
+  // U[2] | ACC | carry[CT][FN] | stab | info[2][CT] | uinfo[2] | fbuf[2][CT*D] (int4)
   double *ACC = smem + 2 * CND;
-  double *carry0 = ACC + CND;                                 // per pencil, read before written
-  double *stab = carry0 + CT * G::FN;                         // xi[8], w[8]
-  CellInfo *info = reinterpret_cast<CellInfo *>(stab + 16);   // [CT]
-  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info + CT);  // [2]
+  double *carry0 = ACC + CND;                                  // per pencil, read before written
+  double *stab = carry0 + CT * G::FN;                          // xi[8], w[8]
+  CellInfo *info0 = reinterpret_cast<CellInfo *>(stab + 16);   // [2][CT]
+  UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info0 + 2 * CT);  // [2]
+  int4 *fbuf = reinterpret_cast<int4 *>((reinterpret_cast<uintptr_t>(uinfo + 2) + 15) & ~uintptr_t(15));
+  // fbuf: [CT * D] fetched flag words (16-byte cp.async destinations)
   const int tid = threadIdx.x;
   const int k = tid / G::NT;
   const int r = tid - k * G::NT;
@@ -751,6 +766,26 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   auto first_cell = [&](int uu, int g, const UnitInfo &ui) {
     return p.pencil ? ui.base + step_group(p, g, ui.dir0, ui.skew) : uu * CT;
   };
+  // decode a group into inf and fetch the flag words its publication checks need (item = (cell, dim))
+  auto decode_group = [&](int uu, int g, const UnitInfo &ui, CellInfo *inf) {
+    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
+      const int kk = idx / D, i = idx - kk * D;
+      decode_cell<D>(p, ui, uu, g, kk, inf[kk], i);
+      const int pf = inf[kk].pflag[i];
+      if (pf >= 0) cp_async16(fbuf + idx, p.flags + (pf & ~3));
+    }
+    cp_async_commit();
+  };
+  auto resolve_group = [&](CellInfo *inf) {
+    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
+      const int kk = idx / D, i = idx - kk * D;
+      const int pf = inf[kk].pflag[i];
+      if (pf < 0) continue;
+      const int4 w = fbuf[idx];
+      const int q = pf & 3;
+      resolve_cell(p, inf[kk], i, q == 0 ? w.x : q == 1 ? w.y : q == 2 ? w.z : w.w);
+    }
+  };
 
   int u = blockIdx.x, gi = 0, it = 0, ju = 0;
   if (p.pencil) {
@@ -758,16 +793,24 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     if (tid >= 32 && tid < 32 + D && u + (int)gridDim.x < p.nunits) decode_unit<D>(p, u + gridDim.x, tid - 32, uinfo[1]);
     __syncthreads();
   }
+  decode_group(u, 0, uinfo[0], info0);
   copy_cells(first_cell(u, 0, uinfo[0]), smem);
   cp_async_commit();
+  cp_async_wait<0>();
+  resolve_group(info0);
   int prev_unit = -1, prev_step = 0;
   while (u < p.nunits) {
+    const int s = it & 1;
+    CellInfo *info = info0 + s * CT;
     int un = u, gn = gi + 1;
     if (gn >= p.GPU) {
       un = u + gridDim.x;
       gn = 0;
     }
-    __syncthreads();  // previous group finished: info, carry, ACC and the other U buffer are free
+    const bool has_next = un < p.nunits;
+    // group g-1 done; this group's cells, decode and flag checks are complete (waited by every thread
+    // before this barrier)
+    __syncthreads();
     if (prev_unit >= 0 && tid == (int)blockDim.x - 1) {
       // the previous group's traces are all written (barrier above): publish its progress
       __threadfence();
@@ -779,29 +822,37 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       if (tid < D && u2 < p.nunits) decode_unit<D>(p, u2, tid, uinfo[(ju + 1) & 1]);
       if (p.GPU == 1) __syncthreads();  // needed right below by the prefetch
     }
-    if (un < p.nunits) copy_cells(first_cell(un, gn, uinfo[(ju + (gn == 0 ? 1 : 0)) & 1]), smem + ((it + 1) & 1) * CND);
+    const UnitInfo &ui_next = uinfo[(ju + (gn == 0 ? 1 : 0)) & 1];
+    if (has_next) copy_cells(first_cell(un, gn, ui_next), smem + (s ^ 1) * CND);
     cp_async_commit();
-    for (int idx = tid; idx < CT * D; idx += blockDim.x) {
-      const int kk = idx / D;
-      decode_cell<D>(p, uinfo[ju & 1], u, gi, kk, info[kk], idx - kk * D);
-    }
-    cp_async_wait<1>();
-    __syncthreads();
     GroupBufs gb;
-    gb.U = smem + (it & 1) * CND;
+    gb.U = smem + s * CND;
     gb.ACC = ACC;
     gb.carry_in = carry0 + (size_t)(active ? k : 0) * G::FN;
     gb.carry_out = carry0 + (size_t)(active ? k : 0) * G::FN;
     const CellInfo &ci = info[active ? k : 0];
-    run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
-    if constexpr (G::NPH > 1) {
-      __syncthreads();
-      run_phase<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+    auto next_decode = [&]() {
+      if (has_next) decode_group(un, gn, ui_next, info0 + (s ^ 1) * CT);
+    };
+    if constexpr (NPH == 1) {
+      next_decode();
+      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+    } else {
+      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+      if constexpr (NPH == 2) {
+        __syncthreads();
+        next_decode();
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+      } else {
+        __syncthreads();
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+        __syncthreads();
+        next_decode();
+        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, gb, active);
+      }
     }
-    if constexpr (G::NPH > 2) {
-      __syncthreads();
-      run_phase<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, gb, active);
-    }
+    cp_async_wait<0>();  // next cells, next flags (and this group's dU)
+    if (has_next) resolve_group(info0 + (s ^ 1) * CT);
     prev_unit = p.pubany ? u : -1;
     prev_step = gi;
     if (gn == 0) ++ju;
@@ -809,7 +860,6 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     gi = gn;
     ++it;
   }
-  cp_async_wait<0>();
   if (prev_unit >= 0) {
     __syncthreads();
     if (tid == (int)blockDim.x - 1) {
