@@ -118,6 +118,9 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.pencil = g.pencil;
   p.UC = g.pencil ? (int)m->pt.len[0] * g.CT : g.CT;
   p.FN = (int)(m->nd / m->n);
+  p.ND = (int)m->nd;
+  p.prefetch = (m->nd * 8) % 16 == 0 ? 1 : 0;
+  if (const char *e = getenv("HD_PREFETCH")) p.prefetch = p.prefetch && atoi(e) != 0;
   p.nunits = m->nunits;
   p.jdet = m->jdet;
   int lstride = 1, ustride = 1;
@@ -152,6 +155,10 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   if (const char *e = getenv("HD_SKEW")) p.skew = g.pencil ? std::min(atoi(e), g.GPU - 1) : 0;
   p.discard = 1;
   if (const char *e = getenv("HD_DISCARD")) p.discard = atoi(e) != 0;
+  p.dbg = 0;
+  if (const char *e = getenv("HD_DBG")) p.dbg = atoi(e);
+  p.pubmode = 0;
+  if (const char *e = getenv("HD_PUBMODE")) p.pubmode = atoi(e);
   next_epoch(m, p, nullptr);
 }
 

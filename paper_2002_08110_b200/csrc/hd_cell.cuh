@@ -110,6 +110,10 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Bring a whole neighbour cell (contiguous, 16-byte multiple) into L2 ahead of a direct read.
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void discard_l2_line(const void *p) {
   asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
 }
@@ -325,6 +329,8 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
     const int kn = (p.pencil && i == 1) ? (k + up + p.CT) % p.CT : k;
     slot = pflag * p.UC + (p.pencil ? kn * p.L[0] + c[0] : kn);
   }
+  if (src == kSrcDirect && pflag < 0 && p.prefetch)
+    prefetch_l2(p.u + (size_t)nb * p.ND, (unsigned)(p.ND * 8));
   ci.src[i] = src;
   ci.out[i] = out;
   ci.nb[i] = nb;
@@ -341,6 +347,8 @@ __device__ __forceinline__ void resolve_cell(const CellParams &p, CellInfo &ci, 
   if (ci.pflag[i] >= 0 && fv >= ci.need[i]) {
     ci.src[i] = kSrcPub;
     ci.tsrc[i] = p.tbuf[i] + (size_t)ci.slot[i] * p.FN;
+  } else if (ci.pflag[i] >= 0 && p.prefetch) {
+    prefetch_l2(p.u + (size_t)ci.nb[i] * p.ND, (unsigned)(p.ND * 8));  // will be read directly
   }
 }
 
@@ -410,13 +418,18 @@ __device__ __forceinline__ void pass_P(double (&acc)[N][N], const double (&uv)[N
       for (int j = 1; j < N; ++j) tr = fma(T.tau[S][j], uv[j][b], tr);
       t[b] = tr;
     }
+    // j outer, a inner: N independent accumulation chains per step (latency-friendly order)
+    double y[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) y[a] = T.K[S][a][0] * uv[0][b];
+#pragma unroll
+    for (int j = 1; j < N; ++j)
+#pragma unroll
+      for (int a = 0; a < N; ++a) y[a] = fma(T.K[S][a][j], uv[j][b], y[a]);
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-      double y = T.K[S][a][0] * uv[0][b];
-#pragma unroll
-      for (int j = 1; j < N; ++j) y = fma(T.K[S][a][j], uv[j][b], y);
-      if constexpr (INIT) acc[a][b] = sb * y;
-      else acc[a][b] = fma(sb, y, acc[a][b]);
+      if constexpr (INIT) acc[a][b] = sb * y[a];
+      else acc[a][b] = fma(sb, y[a], acc[a][b]);
     }
   }
 }
@@ -434,13 +447,15 @@ __device__ __forceinline__ void pass_Q(double (&acc)[N][N], const double (&uv)[N
       for (int j = 1; j < N; ++j) tr = fma(T.tau[S][j], uv[a][j], tr);
       t[a] = tr;
     }
+    double y[N];
 #pragma unroll
-    for (int b = 0; b < N; ++b) {
-      double y = T.K[S][b][0] * uv[a][0];
+    for (int b = 0; b < N; ++b) y[b] = T.K[S][b][0] * uv[a][0];
 #pragma unroll
-      for (int j = 1; j < N; ++j) y = fma(T.K[S][b][j], uv[a][j], y);
-      acc[a][b] = fma(sa, y, acc[a][b]);
-    }
+    for (int j = 1; j < N; ++j)
+#pragma unroll
+      for (int b = 0; b < N; ++b) y[b] = fma(T.K[S][b][j], uv[a][j], y[b]);
+#pragma unroll
+    for (int b = 0; b < N; ++b) acc[a][b] = fma(sa, y[b], acc[a][b]);
   }
 }
 
@@ -625,10 +640,16 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 
   // in-group neighbours (smem) and direct reads of the upwind neighbour (traces not published in time)
   if (ci.src[P] == kSrcGroup) trace_smem<D, N, SP, SQ>(gb.U + (size_t)ci.nb[P] * G::ND, sR, sgP, tP);
-  else if (ci.src[P] == kSrcDirect) trace_global<D, N, SP, SQ>(p.u + (size_t)ci.nb[P] * G::ND + R, sgP, tP);
+  else if (ci.src[P] == kSrcDirect) {
+    if (p.dbg & 1) { for (int l = 0; l < N; ++l) tP[l] = 0.0; }  // timing experiment only
+    else trace_global<D, N, SP, SQ>(p.u + (size_t)ci.nb[P] * G::ND + R, sgP, tP);
+  }
   if constexpr (QA) {
     if (ci.src[Q] == kSrcGroup) trace_smem<D, N, SQ, SP>(gb.U + (size_t)ci.nb[Q] * G::ND, sR, sgQ, tQ);
-    else if (ci.src[Q] == kSrcDirect) trace_global<D, N, SQ, SP>(p.u + (size_t)ci.nb[Q] * G::ND + R, sgQ, tQ);
+    else if (ci.src[Q] == kSrcDirect) {
+      if (p.dbg & 1) { for (int l = 0; l < N; ++l) tQ[l] = 0.0; }  // timing experiment only
+      else trace_global<D, N, SQ, SP>(p.u + (size_t)ci.nb[Q] * G::ND + R, sgQ, tQ);
+    }
   }
 
   // rank-1 lifts of the upwind traces
@@ -704,8 +725,10 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
         const int o = sidx<D, N>(sR, a * SP + b * SQ);
         double dun = acc[a][b];
         if constexpr (MODE == kModeRK) dun = fma(p.rk_a, A[o], dun);
-        __stcs(p.du + g0 + a * SP + b * SQ, dun);
-        __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, dun, U[o]));
+        if (!(p.dbg & 2)) {  // bit 1: timing experiment without the result stores
+          __stcs(p.du + g0 + a * SP + b * SQ, dun);
+          __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, dun, U[o]));
+        }
       }
   }
 }

@@ -71,6 +71,8 @@ struct CellParams {
   int GPU;                // groups (steps) per unit
   int UC;                 // cells per unit (trace-buffer slot size)
   int FN;                 // n^(d-1): doubles per trace
+  int ND;                 // n^d: doubles per cell
+  int prefetch;           // bulk-prefetch neighbour cells that will be read directly into L2
   int pencil;             // 1: pencil mode
   int pubany;             // some dim publishes traces (unit flags needed)
   int L[kMaxD];           // cells per dim (local box)
@@ -83,6 +85,9 @@ struct CellParams {
   int follow[kMaxD];      // pencil mode, dims >= 1: traversal follows the sign of a_i (depends on slower dims only)
   int skew;               // pencil mode: a pencil starts at group (-skew * sum_j t_j) mod GPU (pencil_decode)
   int discard;            // drop consumed published-trace lines from L2 (no write-back)
+  int dbg;                // timing experiments only (HD_DBG; wrong results): 1 no direct reads, 2 no stores,
+                          // 4 no trace publication
+  int pubmode;            // how progress flags are released (publish_flag)
   double *tbuf[kMaxD];    // trace storage per dim: [unit][cell in unit][n^(d-1)]
   int *flags;             // [nunits] unit completion flags (value = epoch)
   // multi-rank: the local box starts at global cell coordinates coff; along a split x dim
