@@ -315,3 +315,49 @@ def test_aliasing_is_rejected():
         m.apply_advection(u, u)
     with pytest.raises(HDError):
         m.rk_step([u, u, torch.zeros_like(u)], 0, 0.0, 1e-3)
+
+
+DEGENERATE = [
+    # a single cell (every neighbour is the cell itself, periodic)
+    ("one-cell-4d", spec_of(2, 2, 3, [1, 1, 1, 1], [0.0, 0.0, -1.0, -1.0], [1.0, 1.0, 1.0, 1.0],
+                            [0.7, -0.4, 0.3, -0.2])),
+    # length-1 dims mixed with longer ones, pencil mode (6D) and groups across pencils (5D)
+    ("thin-6d", spec_of(3, 3, 3, [3, 1, 2, 1, 2, 2], [0.0] * 6, [1.0] * 6, [0.9, -0.5, 0.4, -0.3, 0.2, -0.6])),
+    ("thin-5d", spec_of(3, 2, 3, [5, 4, 1, 2, 2], [0.0] * 5, [1.0] * 5, [-0.9, 0.5, 0.4, -0.3, 0.2])),
+    # speeds exactly zero in some dims (no flux along them)
+    ("zero-speed-4d", spec_of(2, 2, 3, [3, 2, 2, 3], [0.0] * 4, [1.0] * 4, [0.0, 0.8, 0.0, -0.5])),
+    # k = 1 and k = 5 at the sizes the kernels allow
+    ("k1-6d", spec_of(3, 3, 1, [3, 2, 2, 3, 2, 2], [0.0] * 6, [1.0] * 6, [0.5, -0.4, 0.3, -0.2, 0.6, -0.1])),
+    ("k5-4d", spec_of(2, 2, 5, [2, 3, 2, 2], [0.0] * 4, [1.0] * 4, [0.5, -0.4, 0.3, -0.2])),
+]
+
+
+@pytest.mark.parametrize("name,spec", DEGENERATE, ids=[s[0] for s in DEGENERATE])
+def test_degenerate_meshes(name, spec):
+    """Edge cases of the method: self-neighbours (one cell along a dim), zero speeds, extreme degrees."""
+    torch = _torch()
+    m = mesh(spec)
+    N = m.owned_dofs
+    u = np.random.default_rng(5).uniform(-1, 1, N)
+    ud, vd = dev(u), torch.empty(N, dtype=torch.float64, device="cuda")
+    m.apply_advection(ud, vd)
+    assert_close(host(vd), oracle.apply_advection(spec, u), TOL_APPLY, name + " A")
+    dt = 1e-3
+    bufs = [dev(u), torch.empty_like(ud), torch.empty_like(ud)]
+    sol = m.rk_step(bufs, 0, 0.0, dt, nsteps=10)
+    assert_close(host(bufs[sol]), oracle.rk_steps(spec, u, 0.0, dt, 10), TOL_RK10, name + " rk10")
+
+
+def test_repeated_launches_reuse_flags():
+    """Many launches on one mesh (progress flags carry the launch epoch): results stay exact."""
+    torch = _torch()
+    cfg = configs.CONFIGS["5d"]
+    spec = dict(cfg["spec"], cells=[6, 6, 6, 4, 4])
+    m = mesh(spec)
+    u = inputs.full_vector(spec, cfg["recipe"], configs.seed_of("5d"))
+    ud = dev(u)
+    ref = oracle.apply_advection(spec, u)
+    v = torch.empty_like(ud)
+    for _ in range(7):
+        m.apply_advection(ud, v)
+    assert_close(host(v), ref, TOL_APPLY, "repeated A")
