@@ -116,6 +116,7 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.CT = g.CT;
   p.GPU = g.GPU;
   p.pencil = g.pencil;
+  p.line = g.line;
   p.UC = g.pencil ? (int)m->pt.len[0] * g.CT : g.CT;
   p.FN = (int)(m->nd / m->n);
   p.ND = (int)m->nd;
@@ -284,6 +285,7 @@ hd_status setup_halo(hd_mesh *m) {
 hd_status halo_pack(hd_mesh *m, const double *u, cudaStream_t s) {
   if (m->nsend == 0) return HD_OK;
   hd::PackParams pp;
+  pp.line = m->geo.line;
   pp.u = u;
   pp.out = m->sendbuf;
   pp.cells = m->pack_cells;
@@ -475,7 +477,11 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     delete m;
     return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
   }
-  m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local);
+  {
+    int line = 0;  // kernel variant: HD_LINE=1 selects the line kernel
+    if (const char *e = getenv("HD_LINE")) line = atoi(e) != 0;
+    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, line);
+  }
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / (pt.len[0] * m->geo.CT) : m->ncells_local / m->geo.CT);
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
   if (e != cudaSuccess) {

@@ -73,6 +73,7 @@ struct CellParams {
   int FN;                 // n^(d-1): doubles per trace
   int ND;                 // n^d: doubles per cell
   int prefetch;           // bulk-prefetch neighbour cells that will be read directly into L2
+  int line;               // 1: line kernel (hd_line.cuh; face layout = line index), 0: tile kernel
   int pencil;             // 1: pencil mode
   int pubany;             // some dim publishes traces (unit flags needed)
   int L[kMaxD];           // cells per dim (local box)
@@ -101,6 +102,7 @@ struct CellParams {
 // Halo pack (hd_kernels.cu): traces of the listed cells (entry e: cell index, dim, sign) into
 // out[e][n^(d-1)], face points in the consumer's phase layout.
 struct PackParams {
+  int line;             // face layout of the consuming kernel (1: line index)
   const double *u;
   double *out;
   const int *cells;     // [nent]
@@ -137,9 +139,9 @@ bool cell_kernel_supported(int d, int n);
 // Kernel geometry for (d, n) on a local box with L0 cells along dim 0 and ncells cells: cells per group
 // CT, pencil mode, threads per CTA, dynamic smem bytes, phases.
 struct CellGeometry {
-  int CT, pencil, GPU, threads, smem, phases;
+  int CT, pencil, GPU, threads, smem, phases, line;
 };
-CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells);
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line);
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd

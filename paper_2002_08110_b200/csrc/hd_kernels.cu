@@ -57,6 +57,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 }  // namespace hd
 
 #include "hd_cell.cuh"
+#include "hd_line.cuh"
 
 namespace hd {
 
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
     const int X = ds & 255, S = ds >> 8;
     int sx = 1;
     for (int j = 0; j < X; ++j) sx *= N;
-    const double *src = p.u + (size_t)p.cells[e] * G::ND + face_offset<D, N>(X, f);
+    const double *src = p.u + (size_t)p.cells[e] * G::ND + (p.line ? line_base_rt<D, N>(X, f) : face_offset<D, N>(X, f));
     const double *tau = c_tab[N].tau[S];
     double s = tau[0] * __ldg(src);
 #pragma unroll
@@ -202,13 +203,14 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 namespace {
 
 template <int D, int N>
-CellGeometry geometry_dn(int L0, int L1, long long ncells) {
+CellGeometry geometry_dn(int L0, int L1, long long ncells, int line) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
+  g.line = line;
   const int maxCT = 256 / G::NT;
-  const int kSmemMax = HD_MINB > 1 ? 113 * 1024 : 227 * 1024;
-  auto smem_of = [&](int c) { return cell_smem_bytes<D, N>(c); };
+  const int kSmemMax = line ? 74 * 1024 : (HD_MINB > 1 ? 113 * 1024 : 227 * 1024);
+  auto smem_of = [&](int c) { return line ? line_smem_bytes<D, N>(c) : cell_smem_bytes<D, N>(c); };
   if (L0 <= maxCT && smem_of(L0) <= kSmemMax) {
     // multi-pencil groups: m whole pencils per group
     const long long npen = ncells / L0;
@@ -227,14 +229,14 @@ CellGeometry geometry_dn(int L0, int L1, long long ncells) {
     g.pencil = 1;
     g.GPU = L0;
   }
-  g.threads = ((g.CT * G::NT + 31) / 32) * 32;
+  g.threads = line ? 256 : ((g.CT * G::NT + 31) / 32) * 32;
   g.smem = smem_of(g.CT);
   return g;
 }
 
 template <int D, int N, int MODE>
 cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
-  auto kern = cell_kernel<D, N, MODE>;
+  auto kern = g.line ? line_kernel<D, N, MODE> : cell_kernel<D, N, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
   if (e != cudaSuccess) return e;
   int occ = 0;
@@ -246,10 +248,11 @@ cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
 
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
-  const CellGeometry g = geometry_dn<D, N>(p.L[0], p.L[1], (long long)p.nunits * p.UC);
+  const CellGeometry g = geometry_dn<D, N>(p.L[0], p.L[1], (long long)p.nunits * p.UC, p.line);
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
-  cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  if (p.line) line_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  else cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -365,8 +368,8 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s
   HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells) {
-  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells)
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells, line)
 }
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
   HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)
