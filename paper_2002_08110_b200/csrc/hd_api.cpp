@@ -32,7 +32,7 @@ hd_status cuda_fail(cudaError_t e, const char *what) {
 }
 
 // Carpenter-Kennedy five-stage fourth-order 2N-storage coefficients (reading C13, Williamson form
-// S:507). Checked against the classical order conditions by tests/test_host.py.
+// S:507). Checked against the classical order conditions by tests/test_abi.py and tests/test_oracle_lsrk.py.
 const double kRkA[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
                         -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
 const double kRkB[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,

@@ -23,12 +23,6 @@
 #ifndef HD_MINB
 #define HD_MINB 1
 #endif
-#ifndef HD_PG_INLINE
-#define HD_PG_INLINE __forceinline__
-#endif
-#ifndef HD_DU_HINT
-#define HD_DU_HINT 0  // the L2::cache_hint form of cp.async faulted (illegal instruction) in the 6D RK kernel
-#endif
 
 namespace hd {
 

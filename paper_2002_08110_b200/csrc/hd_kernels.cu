@@ -1,21 +1,13 @@
-// hd_kernels.cu -- sm_100a FP64 kernels of the DG advection hot path.
+// hd_kernels.cu -- sm_100a FP64 kernels of the DG advection hot path and their dispatch.
 //
-// cell_kernel<D,N,MODE> (hd_cell.cuh): the element-centric loop of Alg. 1/Alg. 2, persistent
-// cells per CTA iteration, persistent over batches:
-//   step 1 gather      cp.async of the batch's contiguous n^d-blocks into a 128B-swizzled smem tile
-//                      (double-buffered: the next batch is in flight while this one is computed)
-//   step 2 cell terms  interpolation is the identity (Gauss collocation, C1); the quadrature-point
-//                      operation J^-1 a |J| w_q and the gradient test are folded into
-//                      1D matrices applied line by line (sum factorisation)
-//   step 3 faces       upwind only needs the d upwind neighbours; the own-face
-//                      term is folded into the 1D matrix; the neighbour trace (n-point dot along the
-//                      normal) is read through L1/L2 and lifted with a rank-1 update
-//   step 4 M^-1        exact diagonal under collocation, folded into the 1D matrices
-//   step 5 scatter     coalesced stores of the cell result (+ fused LSRK update in RK mode)
-// Work decomposition: dims are processed in pairs (0,1), (2,3), (4,5) (odd d: last phase has one
-// active dim). In a phase a thread owns an n x n tile of the cell over the pair's two dims at fixed
-// other coordinates and keeps it in registers, so both dims are contracted without smem traffic;
-// the running accumulator moves between phases through a swizzled smem buffer.
+//   cell_kernel<D,N,MODE> (hd_cell.cuh)  the fused element-centric loop of Alg. 1/Alg. 2:
+//                                        A, M^-1 A and the LSRK stage in one persistent kernel
+//   line_kernel<D,N,MODE> (hd_line.cuh)  the same with one dim per pass (HD_LINE=1 variant)
+//   mass_kernel<D,N>                     stand-alone u <- M^-1 u / M u
+//   fill_kernel<D,N>                     seeded synthetic initial data
+//   pack_kernel<D,N>                     outgoing halo traces of a rank
+// Instantiated for d = 2..6 and n = 2..6 where one cell fits the kernel (CGeo::OK); the host picks the
+// group geometry (cells per group, pencil mode) per mesh.
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -39,16 +31,6 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
 __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ unsigned long long evict_first_policy() {
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-// 8-byte cp.async with an L2 eviction-priority hint (streams read exactly once: dU)
-__device__ __forceinline__ void cp_async8_ef(void *smem_dst, const void *gsrc, unsigned long long pol) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int K>

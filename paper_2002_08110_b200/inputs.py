@@ -2,7 +2,7 @@
 
 Counter-based: the value at global DoF g depends only on (seed, g), so any subset of
 cells can be regenerated independently (sampled parity at 6D) and the device-side
-generator ``hd_fill_initial`` (csrc/inputs_gen.cu) implements the same recipe for
+generator ``hd_fill_initial`` (csrc/hd_kernels.cu fill_kernel) implements the same recipe for
 configs whose vectors do not fit host memory comfortably. Node positions use
 ``numpy.polynomial.legendre.leggauss`` (a library routine).
 
