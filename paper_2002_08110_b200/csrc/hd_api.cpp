@@ -480,7 +480,9 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   {
     int line = 0;  // kernel variant: HD_LINE=1 selects the line kernel
     if (const char *e = getenv("HD_LINE")) line = atoi(e) != 0;
-    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, line);
+    // pencil mode needs one dim-0 direction per group: a_0 must not depend on z_1
+    const int pencil_ok = d < 2 || m->desc.a_lin[6 * 0 + 1] == 0.0;
+    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, line, pencil_ok);
   }
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / (pt.len[0] * m->geo.CT) : m->ncells_local / m->geo.CT);
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);

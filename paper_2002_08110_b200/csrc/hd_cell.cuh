@@ -18,7 +18,8 @@
 //     lines (no DRAM write-back). A trace that is not published yet (first groups, round seams, wraps)
 //     is formed from the neighbour cell itself (direct read). Nobody ever waits for another CTA.
 //   * multi-pencil mode (L_0 | CT, small d): a group holds whole pencils; in-group neighbours come
-//     from smem, the rest by direct reads.
+//     from smem, the rest by direct reads. Chunk mode (CT | L_0, when a_0 depends on z_1 and a pencil
+//     does not fit one group) is the same with part of a pencil per group.
 #pragma once
 #ifndef HD_MINB
 #define HD_MINB 1
@@ -299,13 +300,8 @@ __device__ __forceinline__ void decode_cell(const CellParams &p, const UnitInfo 
     src = kSrcHalo;
     const int ls = p.lstride[i];
     slot = p.hslot[i][(cell % ls) + (cell / (ls * p.L[i])) * ls];
-  } else if (i == 0) {
-    if (!p.pencil) {
-      src = kSrcGroup;
-      nb = k + (cn - c[0]);
-    } else if (gi > 0) {
-      src = kSrcCarry;  // the previous step processed the upwind neighbour along dim 0
-    }
+  } else if (i == 0 && p.pencil) {
+    if (gi > 0) src = kSrcCarry;  // the previous step processed the upwind neighbour along dim 0
   } else if (p.pencil && i == 1 && k + up >= 0 && k + up < p.CT) {
     src = kSrcGroup;  // the neighbour pencil is in this group
     nb = k + up;

@@ -141,7 +141,7 @@ bool cell_kernel_supported(int d, int n);
 struct CellGeometry {
   int CT, pencil, GPU, threads, smem, phases, line;
 };
-CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line);
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line, int pencil_ok);
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd

@@ -185,7 +185,7 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 namespace {
 
 template <int D, int N>
-CellGeometry geometry_dn(int L0, int L1, long long ncells, int line) {
+CellGeometry geometry_dn(int L0, int L1, long long ncells, int line, int pencil_ok) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
@@ -200,6 +200,16 @@ CellGeometry geometry_dn(int L0, int L1, long long ncells, int line) {
     for (int c = 1; c * L0 <= maxCT; ++c)
       if (npen % c == 0 && smem_of(c * L0) <= kSmemMax) m = c;
     g.CT = m * L0;
+    g.pencil = 0;
+    g.GPU = 1;
+  } else if (!pencil_ok) {
+    // chunk mode (a_0 depends on z_1, so the pencils of a pencil-mode group would sweep dim 0 in
+    // different directions): a group is CT consecutive cells of one pencil (CT | L0); dim-0 neighbours
+    // outside the group are read directly
+    int CT = 1;
+    for (int c = 1; c <= maxCT; ++c)
+      if (L0 % c == 0 && smem_of(c) <= kSmemMax) CT = c;
+    g.CT = CT;
     g.pencil = 0;
     g.GPU = 1;
   } else {
@@ -230,11 +240,13 @@ cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
 
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
-  const CellGeometry g = geometry_dn<D, N>(p.L[0], p.L[1], (long long)p.nunits * p.UC, p.line);
+  // the host decided the geometry (hd_create_mesh); only the block size and smem follow from it
+  const int threads = p.line ? 256 : ((p.CT * CGeo<D, N>::NT + 31) / 32) * 32;
+  const int smem = p.line ? line_smem_bytes<D, N>(p.CT) : cell_smem_bytes<D, N>(p.CT);
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
-  if (p.line) line_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
-  else cell_kernel<D, N, MODE><<<grid, g.threads, g.smem, s>>>(p);
+  if (p.line) line_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
+  else cell_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -350,8 +362,8 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s
   HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line) {
-  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells, line)
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line, int pencil_ok) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells, line, pencil_ok)
 }
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
   HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)

@@ -329,6 +329,16 @@ DEGENERATE = [
     # k = 1 and k = 5 at the sizes the kernels allow
     ("k1-6d", spec_of(3, 3, 1, [3, 2, 2, 3, 2, 2], [0.0] * 6, [1.0] * 6, [0.5, -0.4, 0.3, -0.2, 0.6, -0.1])),
     ("k5-4d", spec_of(2, 2, 5, [2, 3, 2, 2], [0.0] * 4, [1.0] * 4, [0.5, -0.4, 0.3, -0.2])),
+    # pencils longer than one group: a_0 = v_0 = z_1 (chunk mode: part of a pencil per group, the
+    # pencils of a group would sweep dim 0 in opposite directions) ...
+    ("long-x-2d-vlasov", spec_of(1, 1, 1, [520, 4], [0.0, -1.5], [1.0, 1.5], [0.0, 0.3],
+                                 [[0.0, 1.0], [0.0, 0.0]])),
+    ("long-x-3d-vlasov", spec_of(1, 2, 3, [70, 2, 2], [0.0, -1.0, -1.0], [1.0, 1.0, 1.0], [0.0, 0.3, -0.2],
+                                 [[0.0, 1.0, 0.0], [0.0] * 3, [0.0] * 3])),
+    # ... and a_0 independent of z_1 (pencil mode in 2D/3D, dim-0 carry, following dims)
+    ("long-x-2d-const", spec_of(1, 1, 1, [300, 3], [0.0, 0.0], [1.0, 1.0], [-0.8, 0.6])),
+    ("long-x-3d-pencil", spec_of(2, 1, 3, [70, 4, 2], [0.0, 0.0, -1.0], [1.0, 1.0, 1.0], [0.0, 0.4, 0.3],
+                                 [[0.0, 0.0, 1.0], [0.0] * 3, [0.0] * 3])),
 ]
 
 
