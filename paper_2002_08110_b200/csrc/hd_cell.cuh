@@ -30,43 +30,81 @@ namespace hd {
 enum TraceSrc : unsigned char { kSrcDirect = 0, kSrcGroup = 1, kSrcCarry = 2, kSrcPub = 3, kSrcHalo = 4 };
 enum TraceOut : unsigned char { kOutNone = 0, kOutCarry = 1, kOutPub = 2 };
 
+// Shared-memory layout of a cell: element (d_0, ..., d_{D-1}) at sum_i d_i S_i -- ADDITIVE, so a thread's
+// tile element is its rest offset plus a compile-time constant (base + immediate addressing, no
+// per-element index arithmetic). The padded strides (tools/smem_layout.py; pinned by
+// tests/test_smem_layout.py) keep the layout injective (mixed radix), keep 16-byte pairs along dim 0
+// aligned (N even: S_i even for i >= 1) and make the tile accesses of every phase as conflict-free as
+// the earlier XOR swizzle or better; other (D, N) keep the plain strides N^i.
+struct CellStrides {
+  int s[kMaxD];
+};
+template <int D, int N>
+__host__ __device__ constexpr CellStrides cell_strides() {
+  if constexpr (D == 3 && N == 4) return {{1, 4, 18}};
+  else if constexpr (D == 3 && N == 5) return {{1, 5, 28}};
+  else if constexpr (D == 4 && N == 4) return {{1, 4, 18, 76}};
+  else if constexpr (D == 4 && N == 5) return {{1, 5, 25, 136}};
+  else if constexpr (D == 5 && N == 2) return {{1, 2, 4, 8, 18}};
+  else if constexpr (D == 5 && N == 3) return {{1, 3, 9, 27, 88}};
+  else if constexpr (D == 5 && N == 4) return {{1, 4, 18, 76, 298}};
+  else if constexpr (D == 5 && N == 5) return {{1, 5, 25, 133, 665}};
+  else if constexpr (D == 6 && N == 2) return {{1, 2, 4, 8, 18, 36}};
+  else if constexpr (D == 6 && N == 3) return {{1, 3, 9, 27, 81, 245}};
+  else if constexpr (D == 6 && N == 4) return {{1, 4, 18, 76, 298, 1192}};
+  else {
+    CellStrides r{};
+    int m = 1;
+    for (int i = 0; i < D; ++i) {
+      r.s[i] = m;
+      m *= N;
+    }
+    return r;
+  }
+}
+// doubles per cell in shared memory (even when N is even: 16-byte aligned cells)
+template <int D, int N>
+__host__ __device__ constexpr int cell_span() {
+  constexpr CellStrides S = cell_strides<D, N>();
+  int m = 0;
+  for (int i = 0; i < D; ++i) m += (N - 1) * S.s[i];
+  m += 1;
+  return (N % 2 == 0 && m % 2) ? m + 1 : m;
+}
+
 template <int D, int N>
 struct CGeo {
   static constexpr int ND = ipow(N, D);
+  static constexpr int NDP = cell_span<D, N>();  // smem doubles per cell (padded layout)
   static constexpr int FN = ipow(N, D - 1);   // face points per face
   static constexpr int NT = ipow(N, D - 2);   // threads per cell
   static constexpr int NPH = (D + 1) / 2;     // phases
   // phase ph works on the dim pair (P, Q): (0, D-1), (1, 2), (3, 4); QA false: Q already done
   static constexpr __host__ __device__ int P(int ph) { return ph == 0 ? 0 : 2 * ph - 1; }
-  static constexpr __host__ __device__ int Q(int ph) { return ph == 0 ? D - 1 : 2 * ph; }
   static constexpr __host__ __device__ bool QA(int ph) { return ph == 0 || 2 * ph != D - 1; }
-  // one cell must fit the smem pipeline (cell_smem_bytes with CT = 1): n^d <= 4096
-  static constexpr bool OK = NT <= 256 && (5 * ND + NPH * 2 * FN + FN + 16) * 8 + 1024 <= 227 * 1024;
+  static constexpr __host__ __device__ int Q(int ph) { return ph == 0 ? D - 1 : 2 * ph; }
+  // one cell must fit the smem pipeline (cell_smem_bytes with CT = 1; cell info etc. < 2 KB): n^d <= 4096
+  static constexpr bool OK = NT <= 256 && (3 * NDP + FN + 16) * 8 + 2048 + 1024 <= 227 * 1024;
 };
 
-// Shared-memory element order of a cell (n = 4, d >= 4): XOR swizzle of bits 1..3 with bits 4, 6, 7.
-// A bijection that keeps (2e, 2e+1) pairs together (16-byte cp.async / LDS.128) and makes every phase's
-// tile access bank-conflict free (d = 4..6, checked over all phases). It is LINEAR over GF(2):
-// swz(R + T) = swz(R) ^ swz(T) for disjoint digit fields, so a thread's tile element sits at
-// swz(R) ^ (compile-time constant): one LOP3 per element, no per-element index arithmetic.
+// smem position of cell-local element x (runtime digits)
 template <int D, int N>
 __host__ __device__ __forceinline__ constexpr int swz(int x) {
-  if constexpr (N == 4 && D >= 4) {
-    return x ^ (((x >> 6) & 3) << 2) ^ (((x >> 4) & 1) << 1);
-  } else {
-    return x;
+  constexpr CellStrides S = cell_strides<D, N>();
+  int p = 0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    p += (x % N) * S.s[i];
+    x /= N;
   }
+  return p;
 }
 
-// element T (disjoint digit fields from the thread's rest offset R, sR = swz(R)) of a cell buffer:
-// XOR of swizzled fields when n is a power of two (digits are bit fields), plain sum otherwise
+// element T (a compile-time offset whose digits are disjoint from the thread's rest offset R,
+// sR = swz(R)) of a cell buffer: the layout is additive, so this folds to sR + constant
 template <int D, int N>
 __device__ __forceinline__ constexpr int sidx(int sR, int T) {
-  if constexpr ((N & (N - 1)) == 0) {
-    return sR ^ swz<D, N>(T);
-  } else {
-    return sR + T;
-  }
+  return sR + swz<D, N>(T);
 }
 
 struct CellInfo {
@@ -553,8 +591,8 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   thread_phase<D, N, PH, LAST && MODE == kModeAdvection>(p, r, stab, stab + 8, tp);
   const int R = tp.R;
   const int sR = swz<D, N>(R);
-  const double *U = gb.U + (size_t)k * G::ND;
-  double *A = gb.ACC + (size_t)k * G::ND;
+  const double *U = gb.U + (size_t)k * G::NDP;
+  double *A = gb.ACC + (size_t)k * G::NDP;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
   const size_t g0 = (size_t)ci.cell * G::ND + R;
   // line speeds (a_i / h_i) * dtfac = s0 + sl * xi_line (a_i varies only with the other dims)
@@ -629,13 +667,13 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   }
 
   // in-group neighbours (smem) and direct reads of the upwind neighbour (traces not published in time)
-  if (ci.src[P] == kSrcGroup) trace_smem<D, N, SP, SQ>(gb.U + (size_t)ci.nb[P] * G::ND, sR, sgP, tP);
+  if (ci.src[P] == kSrcGroup) trace_smem<D, N, SP, SQ>(gb.U + (size_t)ci.nb[P] * G::NDP, sR, sgP, tP);
   else if (ci.src[P] == kSrcDirect) {
     if (p.dbg & 1) { for (int l = 0; l < N; ++l) tP[l] = 0.0; }  // timing experiment only
     else trace_global<D, N, SP, SQ>(p.u + (size_t)ci.nb[P] * G::ND + R, sgP, tP);
   }
   if constexpr (QA) {
-    if (ci.src[Q] == kSrcGroup) trace_smem<D, N, SQ, SP>(gb.U + (size_t)ci.nb[Q] * G::ND, sR, sgQ, tQ);
+    if (ci.src[Q] == kSrcGroup) trace_smem<D, N, SQ, SP>(gb.U + (size_t)ci.nb[Q] * G::NDP, sR, sgQ, tQ);
     else if (ci.src[Q] == kSrcDirect) {
       if (p.dbg & 1) { for (int l = 0; l < N; ++l) tQ[l] = 0.0; }  // timing experiment only
       else trace_global<D, N, SQ, SP>(p.u + (size_t)ci.nb[Q] * G::ND + R, sgQ, tQ);
@@ -693,7 +731,13 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     }
   }
 
-  if constexpr (!LAST) {
+  if constexpr (!LAST && P == 0 && N % 2 == 0) {
+#pragma unroll
+    for (int b = 0; b < N; ++b)
+#pragma unroll
+      for (int a = 0; a < N; a += 2)
+        *reinterpret_cast<double2 *>(A + sidx<D, N>(sR, a + b * SQ)) = make_double2(acc[a][b], acc[a + 1][b]);
+  } else if constexpr (!LAST) {
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
@@ -726,7 +770,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * G::ND + CT * G::FN + 16) * 8 + 2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo) +
+  return (3 * CT * G::NDP + CT * G::FN + 16) * 8 + 2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo) +
          CT * D * 16 + 16;
 }
 
@@ -741,7 +785,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   constexpr int NPH = G::NPH;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int CT = p.CT;
-  const int CND = CT * G::ND;
+  const int CND = CT * G::NDP;
   double *smem = reinterpret_cast<double *>(smem_raw);
   // U[2] | ACC | carry[CT][FN] | stab | info[2][CT] | uinfo[2] | fbuf[2][CT*D] (int4)
   double *ACC = smem + 2 * CND;
@@ -765,14 +809,14 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   const size_t cs = p.pencil ? (size_t)p.lstride[1] : 1;
   auto copy_cells = [&](int first_cell, double *dst) {
     if constexpr (G::ND % 2 == 0) {
-      for (int i = tid; i < (CND >> 1); i += blockDim.x) {
+      for (int i = tid; i < ((CT * G::ND) >> 1); i += blockDim.x) {
         const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
-        cp_async16(dst + kc * G::ND + swz<D, N>(x), p.u + ((size_t)first_cell + kc * cs) * G::ND + x);
+        cp_async16(dst + kc * G::NDP + swz<D, N>(x), p.u + ((size_t)first_cell + kc * cs) * G::ND + x);
       }
     } else {
-      for (int i = tid; i < CND; i += blockDim.x) {
+      for (int i = tid; i < CT * G::ND; i += blockDim.x) {
         const int kc = i / G::ND, x = i - kc * G::ND;
-        cp_async8(dst + i, p.u + ((size_t)first_cell + kc * cs) * G::ND + x);
+        cp_async8(dst + kc * G::NDP + swz<D, N>(x), p.u + ((size_t)first_cell + kc * cs) * G::ND + x);
       }
     }
   };
