@@ -154,7 +154,7 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   // margin; the first `skew` steps of a pencil then read their upwind neighbours directly
   p.skew = g.pencil && g.GPU > 2 ? 2 : (g.pencil && g.GPU > 1 ? 1 : 0);
   if (const char *e = getenv("HD_SKEW")) p.skew = g.pencil ? std::min(atoi(e), g.GPU - 1) : 0;
-  p.discard = 1;
+  p.discard = 0;  // measured: the discard instructions cost more than the write-back they save (HD_DISCARD=1)
   if (const char *e = getenv("HD_DISCARD")) p.discard = atoi(e) != 0;
   p.dbg = 0;
   if (const char *e = getenv("HD_DBG")) p.dbg = atoi(e);

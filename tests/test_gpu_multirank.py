@@ -43,6 +43,9 @@ CASES = [
     ("5d-vlasov-P8", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 8, None),
     ("5d-vlasov-P3-x0", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 3, [3, 1, 1]),
     ("6d-vlasov-P8", _vlasov(3, 3, 3, [4, 4, 4, 2, 2, 2]), 8, None),
+    # long pencils with a_0 = v_0 = z_1: chunk mode (parts of a pencil per group) with the dim-0 halo
+    ("2d-vlasov-chunk-P2", _vlasov(1, 1, 1, [1040, 4]), 2, None),
+    ("3d-vlasov-chunk-P2", _vlasov(1, 2, 3, [140, 2, 2]), 2, None),
 ]
 
 

@@ -19,11 +19,14 @@ for c in 6d 5d; do
     --clock-control none -k regex:cell_kernel -s 6 -c 2 --csv --log-file $O/traffic_$c.csv \
     python tools/prof_driver.py --config $c --op rk --reps 2 > $O/ncu_traffic_$c.log 2>&1; echo "traffic $c rc=$?"
 done
-# one full capture of the dominant kernel (5D: the 6D replay has to save/restore 140 GB per pass)
-tag=full_5d
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:cell_kernel -s 6 -c 1 \
-   -o $O/ncu_$tag python tools/prof_driver.py --config 5d --op rk --reps 2 > $O/ncu_$tag.log 2>&1
-python tools/ncu_summary.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_$tag.txt 2>&1
-sz=$(stat -c %s $O/ncu_$tag.ncu-rep 2>/dev/null || echo 0)
-if [ "$sz" -gt 50000000 ]; then rm -f $O/ncu_$tag.ncu-rep; fi
+# one full capture of the dominant kernel per headline config (RK stage, steady state)
+for c in 6d 5d; do
+  tag=full_$c
+  timeout 1500 ncu --set full --import-source on --clock-control none -k regex:cell_kernel -s 6 -c 1 \
+     -o $O/ncu_$tag python tools/prof_driver.py --config $c --op rk --reps 2 > $O/ncu_$tag.log 2>&1
+  python tools/ncu_summary.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_$tag.txt 2>&1
+  python tools/ncu_lines.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_${tag}_lines.txt 2>&1
+  sz=$(stat -c %s $O/ncu_$tag.ncu-rep 2>/dev/null || echo 0)
+  if [ "$sz" -gt 20000000 ]; then rm -f $O/ncu_$tag.ncu-rep; fi
+done
 du -sh $O
