@@ -84,20 +84,20 @@ struct CGeo {
   static constexpr __host__ __device__ bool QA(int ph) { return ph == 0 || 2 * ph != D - 1; }
   static constexpr __host__ __device__ int Q(int ph) { return ph == 0 ? D - 1 : 2 * ph; }
   // one cell must fit the smem pipeline (cell_smem_bytes with CT = 1; cell info etc. < 2 KB): n^d <= 4096
-  static constexpr bool OK = NT <= 256 && (3 * NDP + FN + 16) * 8 + 2048 + 1024 <= 227 * 1024;
+  static constexpr bool OK = NT <= 256 && (3 * NDP + FN + 16 + NPH * 1024) * 8 + 2048 + 1024 <= 227 * 1024;
 };
 
 // smem position of cell-local element x (runtime digits)
 template <int D, int N>
 __host__ __device__ __forceinline__ constexpr int swz(int x) {
   constexpr CellStrides S = cell_strides<D, N>();
-  int p = 0;
+  unsigned ux = (unsigned)x, p = 0;  // unsigned: digit extraction is a mask and a shift for N = 2^m
 #pragma unroll
   for (int i = 0; i < D; ++i) {
-    p += (x % N) * S.s[i];
-    x /= N;
+    p += (ux % N) * (unsigned)S.s[i];
+    ux /= N;
   }
-  return p;
+  return (int)p;
 }
 
 // element T (a compile-time offset whose digits are disjoint from the thread's rest offset R,
@@ -576,8 +576,30 @@ struct GroupBufs {
   double *carry_out;
 };
 
+// The per-thread constants of every phase (thread_phase, plus the swizzled rest offset), once per
+// launch into this thread's column of the smem table read by run_phase.
 template <int D, int N, int MODE, int PH>
-__device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *stab, int k, int r,
+__device__ __forceinline__ void phase_entry(const CellParams &p, int r, double *ptab) {
+  using G = CGeo<D, N>;
+  ThreadPhase tp;
+  thread_phase<D, N, PH, PH == G::NPH - 1 && MODE == kModeAdvection>(p, r, c_tab[N].xi, c_tab[N].w, tp);
+  double *pt = ptab + PH * 1024;
+  const int tid = (int)threadIdx.x;
+  pt[tid] = tp.wP;
+  pt[256 + tid] = tp.wQ;
+  pt[512 + tid] = tp.wr;
+  reinterpret_cast<int2 *>(pt + 768)[tid] = make_int2(tp.R, swz<D, N>(tp.R));
+}
+template <int D, int N, int MODE>
+__device__ __forceinline__ void phase_table(const CellParams &p, int r, double *ptab) {
+  using G = CGeo<D, N>;
+  phase_entry<D, N, MODE, 0>(p, r, ptab);
+  if constexpr (G::NPH > 1) phase_entry<D, N, MODE, (G::NPH > 1 ? 1 : 0)>(p, r, ptab);
+  if constexpr (G::NPH > 2) phase_entry<D, N, MODE, (G::NPH > 2 ? 2 : 0)>(p, r, ptab);
+}
+
+template <int D, int N, int MODE, int PH>
+__device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *ptab, int k, int r,
                                           const GroupBufs &gb, bool active) {
   if (!active) return;  // padding threads of the CTA: only the barriers between phases
   using G = CGeo<D, N>;
@@ -587,10 +609,16 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   constexpr bool FIRST = PH == 0, LAST = PH == G::NPH - 1;
   const Tables1D &T = c_tab[N];
 
+  // per-thread phase constants, computed once per launch (phase_table): [PH][wP | wQ | wr | (R, sR)][256]
   ThreadPhase tp;
-  thread_phase<D, N, PH, LAST && MODE == kModeAdvection>(p, r, stab, stab + 8, tp);
-  const int R = tp.R;
-  const int sR = swz<D, N>(R);
+  const int tid = (int)threadIdx.x;
+  const double *pt = ptab + PH * 1024;
+  tp.wP = pt[tid];
+  tp.wQ = pt[256 + tid];
+  tp.wr = pt[512 + tid];
+  const int2 rs = reinterpret_cast<const int2 *>(pt + 768)[tid];
+  const int R = rs.x;
+  const int sR = rs.y;
   const double *U = gb.U + (size_t)k * G::NDP;
   double *A = gb.ACC + (size_t)k * G::NDP;
   const int sgP = ci.sg[P], sgQ = ci.sg[Q];
@@ -770,7 +798,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 template <int D, int N>
 __host__ __device__ constexpr int cell_smem_bytes(int CT) {
   using G = CGeo<D, N>;
-  return (3 * CT * G::NDP + CT * G::FN + 16) * 8 + 2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo) +
+  return (3 * CT * G::NDP + CT * G::FN + G::NPH * 1024 + 16) * 8 + 2 * CT * (int)sizeof(CellInfo) + 2 * (int)sizeof(UnitInfo) +
          CT * D * 16 + 16;
 }
 
@@ -787,10 +815,11 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   const int CT = p.CT;
   const int CND = CT * G::NDP;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  // U[2] | ACC | carry[CT][FN] | stab | info[2][CT] | uinfo[2] | fbuf[2][CT*D] (int4)
+  // U[2] | ACC | carry[CT][FN] | ptab[NPH][4][256] | stab | info[2][CT] | uinfo[2] | fbuf[2][CT*D] (int4)
   double *ACC = smem + 2 * CND;
   double *carry0 = ACC + CND;                                  // per pencil, read before written
-  double *stab = carry0 + CT * G::FN;                          // xi[8], w[8]
+  double *ptab = carry0 + CT * G::FN;                          // [NPH][4][256] per-thread phase constants
+  double *stab = ptab + NPH * 1024;                            // xi[8], w[8]
   CellInfo *info0 = reinterpret_cast<CellInfo *>(stab + 16);   // [2][CT]
   UnitInfo *uinfo = reinterpret_cast<UnitInfo *>(info0 + 2 * CT);  // [2]
   int4 *fbuf = reinterpret_cast<int4 *>((reinterpret_cast<uintptr_t>(uinfo + 2) + 15) & ~uintptr_t(15));
@@ -804,6 +833,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     stab[8 + tid] = tid < N ? c_tab[N].w[tid] : 0.0;
   }
   if ((int)blockIdx.x >= p.nunits) return;
+  phase_table<D, N, MODE>(p, r, ptab);  // read only by this thread
 
   // the group's cells: CT cells at cell stride cs (adjacent pencils in pencil mode, consecutive else)
   const size_t cs = p.pencil ? (size_t)p.lstride[1] : 1;
@@ -893,19 +923,19 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     };
     if constexpr (NPH == 1) {
       next_decode();
-      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+      run_phase<D, N, MODE, 0>(p, ci, ptab, k, r, gb, active);
     } else {
-      run_phase<D, N, MODE, 0>(p, ci, stab, k, r, gb, active);
+      run_phase<D, N, MODE, 0>(p, ci, ptab, k, r, gb, active);
       if constexpr (NPH == 2) {
         __syncthreads();
         next_decode();
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, ptab, k, r, gb, active);
       } else {
         __syncthreads();
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, stab, k, r, gb, active);
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0)>(p, ci, ptab, k, r, gb, active);
         __syncthreads();
         next_decode();
-        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0)>(p, ci, stab, k, r, gb, active);
+        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0)>(p, ci, ptab, k, r, gb, active);
       }
     }
     cp_async_wait<0>();  // next cells, next flags (and this group's dU)
