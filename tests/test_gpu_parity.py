@@ -335,6 +335,8 @@ DEGENERATE = [
                                  [[0.0, 1.0], [0.0, 0.0]])),
     ("long-x-3d-vlasov", spec_of(1, 2, 3, [70, 2, 2], [0.0, -1.0, -1.0], [1.0, 1.0, 1.0], [0.0, 0.3, -0.2],
                                  [[0.0, 1.0, 0.0], [0.0] * 3, [0.0] * 3])),
+    ("long-x-4d-vlasov", spec_of(1, 3, 3, [20, 2, 2, 2], [0.0, -1.0, -1.0, -1.0], [1.0] * 4,
+                                 [0.0, 0.3, -0.2, 0.1], [[0.0, 1.0, 0.0, 0.0]] + [[0.0] * 4] * 3)),
     # ... and a_0 independent of z_1 (pencil mode in 2D/3D, dim-0 carry, following dims)
     ("long-x-2d-const", spec_of(1, 1, 1, [300, 3], [0.0, 0.0], [1.0, 1.0], [-0.8, 0.6])),
     ("long-x-3d-pencil", spec_of(2, 1, 3, [70, 4, 2], [0.0, 0.0, -1.0], [1.0, 1.0, 1.0], [0.0, 0.4, 0.3],
