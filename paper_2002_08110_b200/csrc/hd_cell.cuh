@@ -7,15 +7,16 @@
 // along dim 0; threads own, per phase, an n x n register tile of a cell over a pair of dims (P, Q).
 //
 // Work units and upwind traces (the part that decides performance; DESIGN.md §6 "Upwind traces"):
-//   * pencil mode (CT | L_0): a unit is the pencil of L_0 cells along dim 0, processed group by group
-//     by ONE CTA upwind -> downwind (a_0 has one sign on the pencil). The dim-0 trace of the group's
-//     upwind-end cell is the previous group's downwind trace, carried in smem.
+//   * pencil mode (CT | L_1, a_0 independent of z_1): a group is CT cells at one c_0 from CT adjacent
+//     pencils, a unit is those pencils, processed group by group by ONE CTA upwind -> downwind (a_0
+//     has one sign on the unit). The dim-0 trace of a cell is the previous group's downwind trace,
+//     carried in smem.
 //   * every other dim whose traversal follows the sign of its speed PUBLISHES its downwind traces
 //     (n^(d-1) values, 1/n of a cell) into a per-dim buffer and a per-unit progress flag. Units are
 //     swept in direction-following order with a skewed start (pencil_decode), so a unit's upwind
-//     neighbours in the same round run exactly one group ahead: when a group starts, the traces it needs
-//     were written one group earlier and are still in L2; the consumer reads them once and discards the
-//     lines (no DRAM write-back). A trace that is not published yet (first groups, round seams, wraps)
+//     neighbours in the same round run `skew` groups ahead: when a group starts, the traces it needs
+//     were written a few groups earlier and are usually still in L2 (optionally discarded after use,
+//     HD_DISCARD). A trace that is not published yet (first groups, skew seams, round seams, wraps)
 //     is formed from the neighbour cell itself (direct read). Nobody ever waits for another CTA.
 //   * multi-pencil mode (L_0 | CT, small d): a group holds whole pencils; in-group neighbours come
 //     from smem, the rest by direct reads. Chunk mode (CT | L_0, when a_0 depends on z_1 and a pencil
