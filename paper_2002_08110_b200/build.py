@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhd.so")
-SOURCES = ["hd_api.cpp", "hd_plan.cpp", "hd_tables.cpp", "hd_kernels.cu"]
-HEADERS = ["hd_internal.h", "hd_cell.cuh", os.path.join("..", "..", "include", "hd.h")]
+SOURCES = ["hd_api.cpp", "hd_plan.cpp", "hd_sched.cpp", "hd_tables.cpp", "hd_kernels.cu"]
+HEADERS = ["hd_internal.h", "hd_cell.cuh", os.path.join("..", "..", "include", "hd.h")]  # every header the sources include
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,9 +40,10 @@ def build(force: bool = False, verbose_ptxas: bool = False, out: str = LIB, defi
     if not force and out == LIB and not needs_build():
         return LIB
     objs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    bdir = os.path.join(HERE, "build", os.path.splitext(os.path.basename(out))[0])
+    os.makedirs(bdir, exist_ok=True)
     for src in SOURCES:
-        obj = os.path.join(HERE, "build", src + ".o")
+        obj = os.path.join(bdir, src + ".o")
         cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-c",
                os.path.join(CSRC, src), "-o", obj, "-I", os.path.join(ROOT, "include")]
         cmd += [f"-D{x}" for x in defines]

@@ -107,112 +107,72 @@ hd_status ensure_tables(hd_mesh *m) {
   return HD_OK;
 }
 
-hd_status next_epoch(hd_mesh *m, hd::CellParams &p, cudaStream_t s);
-
+// Kernel parameters of a mesh (the launch-dependent fields -- vectors, mode, stage coefficients, epoch --
+// are set by launch_stage).
 void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   std::memset(&p, 0, sizeof(p));
-  const int d = m->d;
+  const int d = m->d, n = m->n;
   const hd::CellGeometry &g = m->geo;
   p.CT = g.CT;
   p.GPU = g.GPU;
-  p.pencil = g.pencil;
-  p.line = g.line;
-  p.UC = g.pencil ? (int)m->pt.len[0] * g.CT : g.CT;
   p.FN = (int)(m->nd / m->n);
   p.ND = (int)m->nd;
   p.prefetch = (m->nd * 8) % 16 == 0 ? 1 : 0;
-  if (const char *e = getenv("HD_PREFETCH")) p.prefetch = p.prefetch && atoi(e) != 0;
   p.nunits = m->nunits;
   p.jdet = m->jdet;
-  int lstride = 1, ustride = 1;
+  p.cstride = g.pencil ? m->pt.len[0] : 1;
+  p.sched = m->sched;
+  p.schedc = m->schedc;
+  p.flags = m->flags;
+  p.dtfac = 1.0;
   for (int i = 0; i < d; ++i) {
     p.L[i] = (int)m->pt.len[i];
     p.coff[i] = (int)m->pt.off[i];
-    p.xsplit[i] = i < 3 && m->pt.xparts[i] > 1 ? 1 : 0;
-    if (p.xsplit[i]) {
-      p.hbuf[i] = m->hbuf[i];
-      p.hslot[i] = m->hslot[i];
-    }
-    p.lstride[i] = lstride;
-    lstride *= p.L[i];
-    if (i >= 1) {
-      p.ustride[i] = ustride;
-      ustride *= i == 1 && g.pencil ? p.L[i] / g.CT : p.L[i];
-    }
+    if (i < 3 && m->pt.xparts[i] > 1) p.hbuf[i] = m->hbuf[i];
     p.lo[i] = m->desc.lo[i];
     p.h[i] = m->h[i];
     p.inv_h[i] = 1.0 / m->h[i];
     p.a_const[i] = m->desc.a_const[i];
-    for (int j = 0; j < d; ++j) p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
-    p.pub[i] = m->pub[i];
-    p.follow[i] = m->follow[i];
+    bool var = false;
+    for (int j = 0; j < d; ++j) {
+      p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
+      var = var || p.a_lin[i][j] != 0.0;
+    }
+    p.var[i] = var ? 1 : 0;
     p.tbuf[i] = m->tbuf[i];
-    p.pubany |= m->pub[i];
   }
-  p.flags = m->flags;
-  // skew (steps a same-round producer runs ahead of its consumer): 2 gives the producer a full step of
-  // margin; the first `skew` steps of a pencil then read their upwind neighbours directly
-  p.skew = g.pencil && g.GPU > 2 ? 2 : (g.pencil && g.GPU > 1 ? 1 : 0);
-  if (const char *e = getenv("HD_SKEW")) p.skew = g.pencil ? std::min(atoi(e), g.GPU - 1) : 0;
-  p.discard = 0;  // measured: the discard instructions cost more than the write-back they save (HD_DISCARD=1)
-  if (const char *e = getenv("HD_DISCARD")) p.discard = atoi(e) != 0;
-  p.dbg = 0;
-  if (const char *e = getenv("HD_DBG")) p.dbg = atoi(e);
-  p.pubmode = 0;
-  if (const char *e = getenv("HD_PUBMODE")) p.pubmode = atoi(e);
-  next_epoch(m, p, nullptr);
+  (void)n;
 }
 
-// Upwind-trace plan (DESIGN.md §6 "Upwind traces"). In pencil mode a dim i >= 1 FOLLOWS its speed when a_i
-// depends on slower dims only (its sign is then constant along the traversal of dim i and of all faster
-// dims, so the sweep can go upwind -> downwind); every following dim publishes its downwind traces for
-// the neighbour one group later. HD_TRACE=0 turns publishing off (all upwind traces by direct reads).
-hd_status plan_traces(hd_mesh *m) {
-  const int d = m->d;
-  const hd::CellGeometry &g = m->geo;
-  const long long fn = m->nd / m->n;  // face points
-  bool use = g.pencil && g.GPU <= 1023;
-  if (const char *e = getenv("HD_TRACE")) use = use && atoi(e) != 0;
-  bool any = false;
-  for (int i = 0; i < d; ++i) {
-    m->pub[i] = 0;
-    m->follow[i] = 0;
-    m->tbuf[i] = nullptr;
-    if (i == 0 || !g.pencil || m->pt.len[i] < 2) continue;
-    bool follow = true;
-    for (int j = 0; j < i; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
-    m->follow[i] = follow ? 1 : 0;
-    if (!follow || !use) continue;
-    m->pub[i] = 1;
-    const size_t bytes = (size_t)m->ncells_local * fn * sizeof(double);
-    cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
-    }
-    any = true;
+// The speed-prescaled tables of the constant-speed dims for a launch with time factor dtfac (1 for A,
+// dt for an RK stage): s_i K[s], s_i tau[s], s_i = a_i dtfac / h_i, compact [dim][sign][N][N] / [N]. The
+// line speed is formed exactly as the kernel's line_speed does for a constant field ((a_i + 0) * fac).
+void set_dtfac(hd_mesh *m, hd::CellParams &p, double dtfac) {
+  p.dtfac = dtfac;
+  const int N = m->n;
+  for (int i = 0; i < m->d; ++i) {
+    p.fac[i] = dtfac * p.inv_h[i];
+    for (int j = 0; j < m->d; ++j) p.slin[i][j] = p.a_lin[i][j] * p.h[j] * p.fac[i];
   }
-  m->flags = nullptr;
-  if (any) {
-    const size_t fbytes = (size_t)m->nunits * sizeof(int);
-    cudaError_t e = cudaMalloc(&m->flags, fbytes);
-    if (e == cudaSuccess) e = cudaMemset(m->flags, 0, fbytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(HD_ERR_OOM, "flag buffer: %s", cudaGetErrorString(e));
+  for (int i = 0; i < m->d; ++i) {
+    const double si = p.var[i] ? 1.0 : (p.a_const[i] + 0.0) * (dtfac * p.inv_h[i]);
+    for (int sg = 0; sg < 2; ++sg) {
+      for (int a = 0; a < N; ++a) {
+        for (int j = 0; j < N; ++j) p.Ks[((i * 2 + sg) * N + a) * N + j] = si * m->tab.K[sg][a][j];
+        p.Ts[(i * 2 + sg) * N + a] = si * m->tab.tau[sg][a];
+      }
     }
   }
-  m->epoch = 0;
-  return HD_OK;
 }
 
 // Every cell-kernel launch is a new epoch; unit flags hold (epoch << 10) | steps done. Before the epoch
-// field overflows, the flags are cleared on the stream and the count restarts.
+// field overflows, the flags are cleared on the launch stream (ordered after every earlier launch on it)
+// and the count restarts.
 hd_status next_epoch(hd_mesh *m, hd::CellParams &p, cudaStream_t s) {
   m->epoch += 1;
   if (m->epoch >= (1LL << 20)) {
     if (m->flags) {
-      cudaError_t e = cudaMemsetAsync(m->flags, 0, (size_t)m->nunits * sizeof(int), s);
+      cudaError_t e = cudaMemsetAsync(m->flags, 0, (size_t)m->nflags * sizeof(int), s);
       if (e != cudaSuccess) return cuda_fail(e, "flag reset");
     }
     m->epoch = 1;
@@ -225,6 +185,8 @@ void free_mesh(hd_mesh *m) {
   for (int i = 0; i < 6; ++i)
     if (m->tbuf[i]) cudaFree(m->tbuf[i]);
   if (m->flags) cudaFree(m->flags);
+  if (m->sched) cudaFree(m->sched);
+  if (m->schedc) cudaFree(m->schedc);
   for (int i = 0; i < 3; ++i) {
     if (m->hbuf[i]) cudaFree(m->hbuf[i]);
     if (m->hslot[i]) cudaFree(m->hslot[i]);
@@ -247,6 +209,65 @@ hd_status upload(T **dst, const T *src, size_t count, const char *what) {
     return fail(HD_ERR_OOM, "%s (%zu bytes): %s", what, count * sizeof(T), cudaGetErrorString(e));
   }
   return HD_OK;
+}
+
+// Upwind-trace plan (DESIGN.md §6 "Upwind traces"). In pencil mode a dim i >= 1 FOLLOWS its speed when a_i
+// depends on slower dims only (its sign is then constant along the traversal of dim i and of all faster
+// dims, so the sweep can go upwind -> downwind); every following dim publishes its downwind traces for
+// the neighbour one group later.
+hd_status plan_traces(hd_mesh *m) {
+  const int d = m->d;
+  const hd::CellGeometry &g = m->geo;
+  const long long fn = m->nd / m->n;  // face points
+  const bool use = g.pencil && g.GPU <= 1023;
+  bool any = false;
+  for (int i = 0; i < d; ++i) {
+    m->pub[i] = 0;
+    m->follow[i] = 0;
+    m->tbuf[i] = nullptr;
+    if (i == 0 || !g.pencil || m->pt.len[i] < 2) continue;
+    bool follow = true;
+    for (int j = 0; j < i; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
+    m->follow[i] = follow ? 1 : 0;
+    if (!follow || !use) continue;
+    m->pub[i] = 1;
+    const size_t bytes = (size_t)m->ncells_local * fn * sizeof(double);
+    cudaError_t e = cudaMalloc(&m->tbuf[i], bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HD_ERR_OOM, "trace buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+    }
+    any = true;
+  }
+  m->flags = nullptr;
+  m->nflags = 0;
+  if (any) {
+    // rounded up to whole 16-byte words
+    m->nflags = ((long long)m->nunits + 3) / 4 * 4;
+    const size_t fbytes = (size_t)m->nflags * sizeof(int);
+    cudaError_t e = cudaMalloc(&m->flags, fbytes);
+    if (e == cudaSuccess) e = cudaMemset(m->flags, 0, fbytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HD_ERR_OOM, "flag buffer: %s", cudaGetErrorString(e));
+    }
+  }
+  m->epoch = 0;
+  // skew (steps a same-round producer runs ahead of its consumer): 2 gives the producer a full step of
+  // margin; the first `skew` steps of a pencil then read their upwind neighbours directly
+  m->skew = g.pencil && g.GPU > 2 ? 2 : (g.pencil && g.GPU > 1 ? 1 : 0);
+  return HD_OK;
+}
+
+// Build the static schedule of the cell kernel (hd_sched.cpp) and upload it (after the halo plan: halo
+// sources carry receive-buffer slots).
+hd_status upload_schedule(hd_mesh *m) {
+  std::vector<hd::SchedDim> recs;
+  std::vector<hd::SchedCell> cells;
+  hd::build_schedule(*m, recs, cells);
+  hd_status st = upload(&m->sched, recs.data(), recs.size(), "schedule");
+  if (st == HD_OK) st = upload(&m->schedc, cells.data(), cells.size(), "schedule");
+  return st;
 }
 
 // Halo plan and buffers of a multi-rank mesh (hd_plan.cpp).
@@ -281,17 +302,16 @@ hd_status setup_halo(hd_mesh *m) {
   return st;
 }
 
-// Pack the outgoing traces of u (every stage: the operator input changes).
-hd_status halo_pack(hd_mesh *m, const double *u, cudaStream_t s) {
+// Pack the outgoing traces of u (every stage: the operator input changes) with the launch's speeds.
+hd_status halo_pack(hd_mesh *m, const hd::CellParams &p, const double *u, cudaStream_t s) {
   if (m->nsend == 0) return HD_OK;
   hd::PackParams pp;
-  pp.line = m->geo.line;
   pp.u = u;
   pp.out = m->sendbuf;
   pp.cells = m->pack_cells;
   pp.dimsg = m->pack_dimsg;
   pp.nent = m->nsend;
-  cudaError_t e = hd::launch_pack_kernel(m->d, m->n, pp, s, &m->launches);
+  cudaError_t e = hd::launch_pack_kernel(m->d, m->n, pp, p, s, &m->launches);
   if (e != cudaSuccess) return cuda_fail(e, "halo pack kernel");
   return HD_OK;
 }
@@ -478,11 +498,9 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     return fail(HD_ERR_UNSUPPORTED, "more than 2^31 cells per rank");
   }
   {
-    int line = 0;  // kernel variant: HD_LINE=1 selects the line kernel
-    if (const char *e = getenv("HD_LINE")) line = atoi(e) != 0;
     // pencil mode needs one dim-0 direction per group: a_0 must not depend on z_1
     const int pencil_ok = d < 2 || m->desc.a_lin[6 * 0 + 1] == 0.0;
-    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, line, pencil_ok);
+    m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, pencil_ok);
   }
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / (pt.len[0] * m->geo.CT) : m->ncells_local / m->geo.CT);
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
@@ -492,6 +510,7 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   }
   st = plan_traces(m);
   if (st == HD_OK && desc->nranks > 1) st = setup_halo(m);
+  if (st == HD_OK) st = upload_schedule(m);
   if (st == HD_OK && desc->nranks > 1 && desc->nccl_id) {
     st = load_nccl();
     if (st == HD_OK) {
@@ -521,7 +540,7 @@ hd_status hd_destroy_mesh(hd_mesh *m) {
 hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots) {
   if (!m) return fail(HD_ERR_ARG, "null mesh");
   for (int i = 0; i < m->d; ++i) {
-    if (tmode) tmode[i] = m->pub[i] ? 1 : 0;
+    if (tmode) tmode[i] = m->pub[i] ? 2 : 0;
     if (ring_slots) ring_slots[i] = 0;
   }
   return HD_OK;
@@ -556,6 +575,7 @@ hd_status hd_lsrk_coefficients(double *a, double *b) {
 
 static hd_status mass_impl(hd_mesh *m, double *u, void *stream, int inverse) {
   if (!m || !u) return fail(HD_ERR_ARG, "null argument");
+  if (reinterpret_cast<uintptr_t>(u) % 16 != 0) return fail(HD_ERR_ARG, "u is not 16-byte aligned");
   hd_status st = ensure_tables(m);
   if (st != HD_OK) return st;
   hd::StreamParams p;
@@ -702,13 +722,11 @@ namespace {
 // One fused cell-kernel launch over U (A mode or an RK stage). For nranks > 1 the halo traces of U are
 // packed and exchanged first (NCCL transport), unless the caller did it (loopback group driver).
 hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
-                       double b, double dtfac, bool first_launch, cudaStream_t s, bool exchange) {
-  if (!first_launch) {
-    hd_status st = next_epoch(m, p, s);
-    if (st != HD_OK) return st;
-  }
+                       double b, cudaStream_t s, bool exchange) {
+  hd_status st = next_epoch(m, p, s);
+  if (st != HD_OK) return st;
   if (exchange && m->desc.nranks > 1) {
-    hd_status st = halo_pack(m, U, s);
+    st = halo_pack(m, p, U, s);
     if (st == HD_OK) st = halo_exchange_nccl(m, s);
     if (st != HD_OK) return st;
   }
@@ -718,9 +736,15 @@ hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *d
   p.mode = mode;
   p.rk_a = a;
   p.rk_b = b;
-  p.dtfac = dtfac;
   cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, s, &m->launches, m->grid);
   if (e != cudaSuccess) return cuda_fail(e, "cell kernel");
+  return HD_OK;
+}
+
+// Vectors are device pointers the kernels read and write with 16-byte vector accesses.
+hd_status check_vec(const void *v, const char *what) {
+  if (!v) return fail(HD_ERR_ARG, "null %s", what);
+  if (reinterpret_cast<uintptr_t>(v) % 16 != 0) return fail(HD_ERR_ARG, "%s is not 16-byte aligned", what);
   return HD_OK;
 }
 
@@ -737,7 +761,8 @@ hd_status check_bufs(hd_mesh *m, double *buf[3], int *sol, int nsteps, double dt
   if (!std::isfinite(dt)) return fail(HD_ERR_ARG, "dt not finite");
   const size_t bytes = (size_t)m->owned_dofs * sizeof(double);
   for (int i = 0; i < 3; ++i) {
-    if (!buf[i]) return fail(HD_ERR_ARG, "null buffer %d", i);
+    hd_status st = check_vec(buf[i], "buffer");
+    if (st != HD_OK) return st;
     for (int j = 0; j < i; ++j)
       if (overlaps(buf[i], buf[j], bytes)) return fail(HD_ERR_ARG, "buffers %d and %d overlap", j, i);
   }
@@ -750,14 +775,18 @@ extern "C" {
 
 hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream) {
   (void)t;
-  if (!m || !u || !v) return fail(HD_ERR_ARG, "null argument");
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_vec(u, "u");
+  if (st == HD_OK) st = check_vec(v, "v");
+  if (st != HD_OK) return st;
   if (overlaps(u, v, (size_t)m->owned_dofs * sizeof(double))) return fail(HD_ERR_ARG, "u and v overlap");
-  hd_status st = check_transport(m);
+  st = check_transport(m);
   if (st == HD_OK) st = ensure_tables(m);
   if (st != HD_OK) return st;
   hd::CellParams p;
   fill_cell_params(m, p);
-  return launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, 1.0, true, (cudaStream_t)stream, true);
+  set_dtfac(m, p, 1.0);
+  return launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream, true);
 }
 
 hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {
@@ -769,11 +798,12 @@ hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, 
   if (st != HD_OK) return st;
   hd::CellParams p;
   fill_cell_params(m, p);
+  set_dtfac(m, p, dt);
   int iu = *sol, idu = (*sol + 1) % 3, iw = (*sol + 2) % 3;
   for (int step = 0; step < nsteps; ++step) {
     for (int s = 0; s < 5; ++s) {
       st = launch_stage(m, p, buf[iu], buf[idu], buf[iw], s == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[s], kRkB[s],
-                        dt, step == 0 && s == 0, (cudaStream_t)stream, true);
+                        (cudaStream_t)stream, true);
       if (st != HD_OK) return st;
       std::swap(iu, iw);
     }
@@ -792,16 +822,17 @@ hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double
     if (st != HD_OK) return st;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  std::vector<hd::CellParams> ps(P);
   for (int r = 0; r < P; ++r) {
-    hd_status st = halo_pack(ms[r], u[r], s);
+    fill_cell_params(ms[r], ps[r]);
+    set_dtfac(ms[r], ps[r], 1.0);
+    hd_status st = halo_pack(ms[r], ps[r], u[r], s);
     if (st != HD_OK) return st;
   }
   hd_status st = halo_exchange_loopback(ms, P, s);
   if (st != HD_OK) return st;
   for (int r = 0; r < P; ++r) {
-    hd::CellParams p;
-    fill_cell_params(ms[r], p);
-    st = launch_stage(ms[r], p, u[r], nullptr, v[r], hd::kModeAdvection, 0.0, 0.0, 1.0, true, s, false);
+    st = launch_stage(ms[r], ps[r], u[r], nullptr, v[r], hd::kModeAdvection, 0.0, 0.0, s, false);
     if (st != HD_OK) return st;
   }
   return HD_OK;
@@ -820,20 +851,22 @@ hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double 
   }
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<hd::CellParams> ps(P);
-  for (int r = 0; r < P; ++r) fill_cell_params(ms[r], ps[r]);
+  for (int r = 0; r < P; ++r) {
+    fill_cell_params(ms[r], ps[r]);
+    set_dtfac(ms[r], ps[r], dt);
+  }
   int iu = *sol, idu = (*sol + 1) % 3, iw = (*sol + 2) % 3;
   for (int step = 0; step < nsteps; ++step) {
     for (int st5 = 0; st5 < 5; ++st5) {
       for (int r = 0; r < P; ++r) {
-        hd_status st = halo_pack(ms[r], bufs[3 * r + iu], s);
+        hd_status st = halo_pack(ms[r], ps[r], bufs[3 * r + iu], s);
         if (st != HD_OK) return st;
       }
       hd_status st = halo_exchange_loopback(ms, P, s);
       if (st != HD_OK) return st;
       for (int r = 0; r < P; ++r) {
         st = launch_stage(ms[r], ps[r], bufs[3 * r + iu], bufs[3 * r + idu], bufs[3 * r + iw],
-                          st5 == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[st5], kRkB[st5], dt, step == 0 && st5 == 0,
-                          s, false);
+                          st5 == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[st5], kRkB[st5], s, false);
         if (st != HD_OK) return st;
       }
       std::swap(iu, iw);

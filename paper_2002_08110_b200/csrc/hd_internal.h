@@ -53,10 +53,35 @@ int host_cell_sign(const hd_mesh_desc &ds, const double *h, int d, int i, const 
 bool make_partition(const hd_mesh_desc &ds, Partition &pt, std::string &err);
 void make_halo(const hd_mesh_desc &ds, const Partition &pt, const double *h, int i, HaloDim &hd);
 
-// Kernel parameters of the fused cell kernel (passed by value as __grid_constant__).
-// Work decomposition: pencil mode -- a group = CT cells at one dim-0 position from CT
-// adjacent pencils (CT | L_1), a unit = those CT pencils, one group per step; multi-pencil mode (small
-// d) -- a group = CT consecutive cells holding whole pencils, one group per unit.
+// Static schedule of the fused cell kernel (built on the host by hd_sched.cpp, read by the kernel): one
+// record per (group, cell slot k, dim i), 32 bytes. A group is the CT cells one CTA processes together;
+// groups are numbered unit * GPU + step. Everything about a cell and its upwind traces is decided here
+// once per mesh -- the kernel does no index decoding. The one run-time decision left is whether a
+// published trace is ready (the producer's progress flag), which falls back to a direct read.
+enum TraceSrc : unsigned char { kSrcDirect = 0, kSrcGroup = 1, kSrcCarry = 2, kSrcPub = 3, kSrcHalo = 4 };
+enum TraceOut : unsigned char { kOutNone = 0, kOutCarry = 1, kOutPub = 2 };
+struct SchedDim {
+  double base;            // a_i at the cell's lower corner (global coordinates; speed of the cell's lines
+                          // before the per-node offsets); the sign below is that of a_i on the cell
+  int nb;                 // upwind neighbour cell (local index): kSrcDirect, and the fallback of kSrcPub
+  int slot;               // kSrcGroup: neighbour slot k' in the group; kSrcPub: producer trace slot;
+                          // kSrcHalo: receive-buffer slot
+  int pflag;              // kSrcPub: producer unit whose progress flag is checked (-1: none)
+  int need;               // kSrcPub: producer steps (flag payload) that must be complete
+  unsigned char src, out, sg, pad;  // TraceSrc, TraceOut, 1: a_i < 0 (upwind neighbour at +e_i)
+  int pad2;
+};
+// per (group, cell slot): the cell and the slot its published traces go to
+struct SchedCell {
+  int cell;               // local cell index (memory order)
+  int oslot;              // kOutPub: trace slot of this cell (same index in every dim's buffer)
+};
+static_assert(sizeof(SchedDim) == 32, "SchedDim is 32 bytes");
+
+// Kernel parameters of the fused cell kernel (passed by value as __grid_constant__; > 4 KB, which
+// CUDA >= 12.1 allows). Work decomposition: a group = CT cells (pencil mode: one dim-0
+// position of CT adjacent pencils; else CT consecutive cells), a unit = GPU groups processed in order by
+// one CTA; units are dealt round-robin to the persistent CTAs.
 struct CellParams {
   const double *u;        // operator input (never written by the kernel)
   double *out;            // A-mode: v; RK-mode: U_new
@@ -69,40 +94,32 @@ struct CellParams {
   int nunits;             // units of this launch
   int CT;                 // cells per group
   int GPU;                // groups (steps) per unit
-  int UC;                 // cells per unit (trace-buffer slot size)
-  int FN;                 // n^(d-1): doubles per trace
   int ND;                 // n^d: doubles per cell
-  int prefetch;           // bulk-prefetch neighbour cells that will be read directly into L2
-  int line;               // 1: line kernel (hd_line.cuh; face layout = line index), 0: tile kernel
-  int pencil;             // 1: pencil mode
-  int pubany;             // some dim publishes traces (unit flags needed)
-  int L[kMaxD];           // cells per dim (local box)
-  int lstride[kMaxD];     // cell-index stride per dim (memory order)
-  int ustride[kMaxD];     // unit-index stride per dim (pencil mode, dims >= 1)
-  double lo[kMaxD], h[kMaxD], inv_h[kMaxD];
+  int FN;                 // n^(d-1): doubles per trace
+  int prefetch;           // bulk-prefetch cells that will be read directly into L2
+  long long cstride;      // cell-index stride between the cells of a group (pencil mode: L_0; else 1)
+  const SchedDim *sched;  // [nunits * GPU][CT][D]
+  const SchedCell *schedc;  // [nunits * GPU][CT]
+  int *flags;             // [nunits rounded up to 4] unit progress flags
+  double *tbuf[kMaxD];    // published traces per dim: [slot][n^(d-1)]
+  const double *hbuf[kMaxD];  // received halo traces per x dim: [slot][n^(d-1)]
+  int var[kMaxD];         // 1: a_i depends on z (line speeds vary: u is scaled per line); 0: constant
+  double inv_h[kMaxD], h[kMaxD], lo[kMaxD];
   double a_const[kMaxD];
   double a_lin[kMaxD][kMaxD];
-  int pub[kMaxD];         // 1: dim publishes traces into tbuf (one slot per unit) for its downwind neighbour
-  int follow[kMaxD];      // pencil mode, dims >= 1: traversal follows the sign of a_i (depends on slower dims only)
-  int skew;               // pencil mode: a pencil starts at group (-skew * sum_j t_j) mod GPU (pencil_decode)
-  int discard;            // drop consumed published-trace lines from L2 (no write-back)
-  int dbg;                // timing experiments only (HD_DBG; wrong results): 1 no direct reads, 2 no stores,
-                          // 4 no trace publication
-  int pubmode;            // how progress flags are released (publish_flag)
-  double *tbuf[kMaxD];    // trace storage per dim: [unit][cell in unit][n^(d-1)]
-  int *flags;             // [nunits] unit completion flags (value = epoch)
-  // multi-rank: the local box starts at global cell coordinates coff; along a split x dim
-  // a neighbour outside the box is on another rank and its trace comes from the halo buffer
-  int coff[kMaxD];
-  int xsplit[kMaxD];
-  const double *hbuf[kMaxD];  // received traces per x dim: [slot][n^(d-1)]
-  const int *hslot[kMaxD];    // face-plane position -> slot
+  double fac[kMaxD];      // dtfac / h_i (line speed = (a_i at the line) * fac)
+  double slin[kMaxD][kMaxD];  // a_lin[i][j] h_j fac_i: change of the line speed of dim i per unit node of dim j
+  int coff[kMaxD];        // global cell coordinates of the local box origin (pack kernel)
+  int L[kMaxD];           // local box (pack kernel)
+  // constant-speed dims: s_i K[s] and s_i tau[s] with s_i = a_i dtfac / h_i (compact [dim][sign][N][N]
+  // and [dim][sign][N] for the mesh's N); variable dims use the unit-speed c_tab tables on scaled lines
+  double Ks[kMaxD * 2 * kMaxN * kMaxN];
+  double Ts[kMaxD * 2 * kMaxN];
 };
 
 // Halo pack (hd_kernels.cu): traces of the listed cells (entry e: cell index, dim, sign) into
 // out[e][n^(d-1)], face points in the consumer's phase layout.
 struct PackParams {
-  int line;             // face layout of the consuming kernel (1: line index)
   const double *u;
   double *out;
   const int *cells;     // [nent]
@@ -134,14 +151,18 @@ cudaError_t upload_tables(int n, const Tables1D &t);
 cudaError_t launch_cell_kernel(int d, int n, const CellParams &p, cudaStream_t s, long long *launches, int grid);
 cudaError_t launch_mass_kernel(int d, int n, const StreamParams &p, cudaStream_t s, long long *launches, int sms);
 cudaError_t launch_fill_kernel(int d, int n, const FillParams &p, cudaStream_t s, long long *launches);
-cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s, long long *launches);
+cudaError_t launch_pack_kernel(int d, int n, const PackParams &pp, const CellParams &cp, cudaStream_t s,
+                               long long *launches);
 bool cell_kernel_supported(int d, int n);
+
+// Static schedule of a mesh (hd_sched.cpp): [nunits * GPU][CT][d] records (see SchedDim).
+void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<SchedCell> &cells);
 // Kernel geometry for (d, n) on a local box with L0 cells along dim 0 and ncells cells: cells per group
 // CT, pencil mode, threads per CTA, dynamic smem bytes, phases.
 struct CellGeometry {
-  int CT, pencil, GPU, threads, smem, phases, line;
+  int CT, pencil, GPU, threads, smem, phases;
 };
-CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line, int pencil_ok);
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int pencil_ok);
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid);
 
 }  // namespace hd
@@ -167,8 +188,12 @@ struct hd_mesh {
   hd::CellGeometry geo;
   int nunits;
   int pub[6], follow[6];
+  int skew;                // pencil mode: a unit starts at step (-skew * sum_j t_j) mod GPU (hd_sched.cpp)
   double *tbuf[6];
   int *flags;
+  long long nflags;        // flag words allocated (nunits rounded up to 4)
+  hd::SchedDim *sched;     // device copy of the static schedule
+  hd::SchedCell *schedc;
   long long epoch;
   int grid;
   // halo (nranks > 1): per x dim receive buffer and slot table; one send buffer for all dims, laid

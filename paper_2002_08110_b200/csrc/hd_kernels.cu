@@ -2,7 +2,6 @@
 //
 //   cell_kernel<D,N,MODE> (hd_cell.cuh)  the fused element-centric loop of Alg. 1/Alg. 2:
 //                                        A, M^-1 A and the LSRK stage in one persistent kernel
-//   line_kernel<D,N,MODE> (hd_line.cuh)  the same with one dim per pass (HD_LINE=1 variant)
 //   mass_kernel<D,N>                     stand-alone u <- M^-1 u / M u
 //   fill_kernel<D,N>                     seeded synthetic initial data
 //   pack_kernel<D,N>                     outgoing halo traces of a rank
@@ -39,7 +38,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 }  // namespace hd
 
 #include "hd_cell.cuh"
-#include "hd_line.cuh"
 
 namespace hd {
 
@@ -151,28 +149,64 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillP
 }
 
 // ---------------------------------------------------------------------------------------------
-// Halo pack: the downwind trace of each listed cell along its listed dim, written in the
-// consumer's phase layout (face point f = N r + l: rest digits r, partner tile digit l), with the same
-// summation order as the cell kernel, so a trace that crosses ranks has the bits it would have had
-// inside one rank.
+// Halo pack: the (scaled) downwind trace of each listed cell along its listed dim, written in
+// the consumer's phase layout (face point f = N r + l: rest digits r, partner tile digit l). The line speed
+// and the trace are evaluated with the cell kernel's expressions (line_speed, line_trace), so a trace that
+// crosses ranks has the bits it would have had inside one rank.
 template <int D, int N>
-__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams p) {
+__device__ __forceinline__ double pack_cell_base(const CellParams &p, int X, long long cell) {
+  double ab = p.a_const[X];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const long long c = cell % p.L[j];
+    cell /= p.L[j];
+    ab = fma(p.a_lin[X][j], fma((double)((int)c + p.coff[j]), p.h[j], p.lo[j]), ab);
+  }
+  return ab;
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackParams pp, const __grid_constant__ CellParams p) {
   using G = CGeo<D, N>;
-  const long long total = p.nent * G::FN;
+  const long long total = pp.nent * G::FN;
   for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < total;
        gi += (long long)gridDim.x * blockDim.x) {
     const long long e = gi / G::FN;
     const int f = (int)(gi - e * G::FN);
-    const int ds = p.dimsg[e];
+    const int ds = pp.dimsg[e];
     const int X = ds & 255, S = ds >> 8;
+    // the consumer's phase of dim X, partner dim Y, rest index r and partner digit l of face point f
+    const int ph = (X == 0 || X == D - 1) ? 0 : (X + 1) / 2;
+    const int P = G::P(ph), Q = G::Q(ph);
+    const int Y = X == P ? Q : P;
+    const int r = f / N, l = f - r * N;
+    // rest offset of the speed (thread_phase's sum, same order)
+    double w = 0.0;
+    int rr = r;
+    for (int j = 0; j < D; ++j) {
+      if (j != P && j != Q) {
+        const int m = rr % N;
+        rr /= N;
+        w = fma(p.a_lin[X][j] * p.h[j], c_tab[N].xi[m], w);
+      }
+    }
+    const LineSpeed ls = line_speed(p, X, Y, pack_cell_base<D, N>(p, X, pp.cells[e]), w);
+    const double s = p.var[X] ? fma(ls.sl, c_tab[N].xi[l], ls.s0) : 0.0;
     int sx = 1;
     for (int j = 0; j < X; ++j) sx *= N;
-    const double *src = p.u + (size_t)p.cells[e] * G::ND + (p.line ? line_base_rt<D, N>(X, f) : face_offset<D, N>(X, f));
-    const double *tau = c_tab[N].tau[S];
-    double s = tau[0] * __ldg(src);
+    const double *src = pp.u + (size_t)pp.cells[e] * G::ND + face_offset<D, N>(X, f);
+    // line_trace with a run-time dim
+    double us[N];
 #pragma unroll
-    for (int j = 1; j < N; ++j) s = fma(tau[j], __ldg(src + j * sx), s);
-    p.out[gi] = s;
+    for (int j = 0; j < N; ++j) {
+      const double v = __ldg(src + j * sx);
+      us[j] = p.var[X] ? s * v : v;
+    }
+    const double *tau = p.var[X] ? c_tab[N].tau[S] : p.Ts + (X * 2 + S) * N;
+    double t = tau[0] * us[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j) t = fma(tau[j], us[j], t);
+    pp.out[gi] = t;
   }
 }
 
@@ -184,15 +218,25 @@ cudaError_t upload_tables(int n, const Tables1D &t) {
 
 namespace {
 
+// Kernel instances built: every (d, n) whose cell fits (CGeo::OK). HD_ONLY_BENCH (experiment builds,
+// `python -m paper_2002_08110_b200.build -DHD_ONLY_BENCH --out=...`) keeps only the bench configs.
 template <int D, int N>
-CellGeometry geometry_dn(int L0, int L1, long long ncells, int line, int pencil_ok) {
+constexpr bool built() {
+#ifdef HD_ONLY_BENCH
+  if (!((D == 4 && N == 4) || (D == 5 && N == 4) || (D == 6 && N == 4) || (D == 3 && N == 5))) return false;
+#endif
+  return CGeo<D, N>::OK;
+}
+
+template <int D, int N>
+CellGeometry geometry_dn(int L0, int L1, long long ncells, int pencil_ok) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
-  g.line = line;
   const int maxCT = 256 / G::NT;
-  const int kSmemMax = line ? 74 * 1024 : (HD_MINB > 1 ? 113 * 1024 : 227 * 1024);
-  auto smem_of = [&](int c) { return line ? line_smem_bytes<D, N>(c) : cell_smem_bytes<D, N>(c); };
+  // two CTAs per SM when the group fits half the shared memory (HD_MINB = 2 in the launch bounds)
+  const int kSmemMax = HD_MINB > 1 ? 113 * 1024 : 227 * 1024;
+  auto smem_of = [&](int c) { return cell_smem_bytes<D, N>(c); };
   if (L0 <= maxCT && smem_of(L0) <= kSmemMax) {
     // multi-pencil groups: m whole pencils per group
     const long long npen = ncells / L0;
@@ -221,15 +265,15 @@ CellGeometry geometry_dn(int L0, int L1, long long ncells, int line, int pencil_
     g.pencil = 1;
     g.GPU = L0;
   }
-  g.threads = line ? 256 : ((g.CT * G::NT + 31) / 32) * 32;
+  g.threads = ((g.CT * G::NT + 31) / 32) * 32;
   g.smem = smem_of(g.CT);
   return g;
 }
 
 template <int D, int N, int MODE>
 cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
-  auto kern = g.line ? line_kernel<D, N, MODE> : cell_kernel<D, N, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
+  auto kern = cell_kernel<D, N, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, g.threads, g.smem);
@@ -241,18 +285,17 @@ cudaError_t grid_impl(const CellGeometry &g, int sms, int *grid) {
 template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
   // the host decided the geometry (hd_create_mesh); only the block size and smem follow from it
-  const int threads = p.line ? 256 : ((p.CT * CGeo<D, N>::NT + 31) / 32) * 32;
-  const int smem = p.line ? line_smem_bytes<D, N>(p.CT) : cell_smem_bytes<D, N>(p.CT);
+  const int threads = ((p.CT * CGeo<D, N>::NT + 31) / 32) * 32;
+  const int smem = cell_smem_bytes<D, N>(p.CT);
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
-  if (p.line) line_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
-  else cell_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
+  cell_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 template <int D, int N>
 cudaError_t launch_cell_dn(const CellParams &p, cudaStream_t s, int grid_max) {
-  if constexpr (!CGeo<D, N>::OK) {
+  if constexpr (!built<D, N>()) {
     return cudaErrorNotSupported;
   } else {
     switch (p.mode) {
@@ -265,7 +308,7 @@ cudaError_t launch_cell_dn(const CellParams &p, cudaStream_t s, int grid_max) {
 
 template <int D, int N>
 cudaError_t grid_dn(const CellGeometry &g, int sms, int *grid) {
-  if constexpr (!CGeo<D, N>::OK) {
+  if constexpr (!built<D, N>()) {
     return cudaErrorNotSupported;
   } else {
     // all modes share the geometry; take the minimum co-residency over them
@@ -310,17 +353,17 @@ cudaError_t launch_fill_dn(const FillParams &p, cudaStream_t s) {
 }
 
 template <int D, int N>
-cudaError_t launch_pack_dn(const PackParams &p, cudaStream_t s) {
-  long long total = p.nent * (long long)ipow(N, D - 1);
+cudaError_t launch_pack_dn(const PackParams &pp, const CellParams &p, cudaStream_t s) {
+  long long total = pp.nent * (long long)ipow(N, D - 1);
   long long grid = (total + 255) / 256;
   if (grid > 148LL * 16) grid = 148LL * 16;
   if (grid < 1) return cudaSuccess;
-  pack_kernel<D, N><<<(unsigned)grid, 256, 0, s>>>(p);
+  pack_kernel<D, N><<<(unsigned)grid, 256, 0, s>>>(pp, p);
   return cudaGetLastError();
 }
 
 template <int D, int N>
-bool supported_dn() { return CGeo<D, N>::OK; }
+bool supported_dn() { return built<D, N>(); }
 
 #define HD_DISPATCH_N(D, FN, ...)                  \
   switch (n) {                                     \
@@ -357,13 +400,14 @@ cudaError_t launch_fill_kernel(int d, int n, const FillParams &p, cudaStream_t s
   if (launches) ++*launches;
   HD_DISPATCH(launch_fill_dn, cudaErrorNotSupported, p, s)
 }
-cudaError_t launch_pack_kernel(int d, int n, const PackParams &p, cudaStream_t s, long long *launches) {
+cudaError_t launch_pack_kernel(int d, int n, const PackParams &pp, const CellParams &cp, cudaStream_t s,
+                               long long *launches) {
   if (launches) ++*launches;
-  HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, p, s)
+  HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, pp, cp, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
-CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int line, int pencil_ok) {
-  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells, line, pencil_ok)
+CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int pencil_ok) {
+  HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells, pencil_ok)
 }
 cudaError_t cell_grid_size(int d, int n, const CellGeometry &g, int sms, int *grid) {
   HD_DISPATCH(grid_dn, cudaErrorNotSupported, g, sms, grid)

@@ -373,23 +373,3 @@ def test_repeated_launches_reuse_flags():
     for _ in range(7):
         m.apply_advection(ud, v)
     assert_close(host(v), ref, TOL_APPLY, "repeated A")
-
-
-LINE_CASES = [s for s in SMALL if s[0] in ("d4k3vlasov", "d5k3vlasov", "d6k3vlasov", "d3k4const", "d2k3const")]
-
-
-@pytest.mark.parametrize("name,spec", LINE_CASES, ids=[s[0] for s in LINE_CASES])
-def test_line_kernel_variant(name, spec, monkeypatch):
-    """The line variant of the cell kernel (HD_LINE=1) against the oracle."""
-    torch = _torch()
-    monkeypatch.setenv("HD_LINE", "1")
-    m = mesh(spec)
-    N = m.owned_dofs
-    u = np.random.default_rng(17).uniform(-1, 1, N)
-    ud, vd = dev(u), torch.empty(N, dtype=torch.float64, device="cuda")
-    m.apply_advection(ud, vd)
-    assert_close(host(vd), oracle.apply_advection(spec, u), TOL_APPLY, name + " line A")
-    dt = configs.time_step(spec, 0.1)
-    bufs = [dev(u), torch.empty_like(ud), torch.empty_like(ud)]
-    sol = m.rk_step(bufs, 0, 0.0, dt, nsteps=10)
-    assert_close(host(bufs[sol]), oracle.rk_steps(spec, u, 0.0, dt, 10), TOL_RK10, name + " line rk10")
