@@ -588,9 +588,17 @@ struct SmemMap {
   }
 };
 static_assert(sizeof(CellInfo) % 8 == 0 && sizeof(SchedDim) % 16 == 0 && sizeof(SchedCell) == 8, "smem records");
+// Largest group (cells) the kernel lays out: every smem offset is a compile-time constant for it (a mesh
+// with a smaller group leaves part of the buffers unused).
 template <int D, int N>
-__host__ __device__ constexpr int cell_smem_bytes(int CT) {
-  return SmemMap<D, N>(CT).bytes;
+__host__ __device__ constexpr int max_ct() {
+  int c = 256 / CGeo<D, N>::NT;
+  while (c > 1 && SmemMap<D, N>(c).bytes > 227 * 1024) --c;
+  return c;
+}
+template <int D, int N>
+__host__ __device__ constexpr int cell_smem_bytes() {
+  return SmemMap<D, N>(max_ct<D, N>()).bytes;
 }
 
 // Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
@@ -604,9 +612,10 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   constexpr int NPH = G::NPH;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int CT = p.CT;
-  const int CND = CT * G::NDP;
+  constexpr int MAXCT = max_ct<D, N>();
+  constexpr int CND = MAXCT * G::NDP;
   double *smem = reinterpret_cast<double *>(smem_raw);
-  const SmemMap<D, N> map(CT);
+  constexpr SmemMap<D, N> map(MAXCT);
   double *bufs = smem;
   double *carry0 = smem + map.carry;
   double *ptab = smem + map.ptab;
@@ -624,8 +633,32 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   phase_table<D, N, MODE>(p, r, ptab);  // read only by this thread
   const int nitems = CT * D;
 
-  // the group's cells: CT cells at cell stride cstride into the padded layout
+  // the group's cells: CT cells at cell stride cstride into the padded layout, 16-byte cp.async per pair
+  // of dim-0 neighbours. Fast path (N = 4, 256 threads, CT n^d a multiple of 512): thread tid copies the
+  // pairs x = 2 tid + 512 j, whose smem position is additive in (tid, j) -- swz(2 tid mod n^d) once per
+  // launch plus a compile-time offset (no digit carries between the two parts for N = 4).
+  constexpr bool FASTFILL = N == 4 && G::NT * MAXCT == 256 && (G::ND % 512 == 0 || 512 % G::ND == 0);
+  const int fbase = swz<D, N>((2 * tid) % G::ND);
+  const int fcell0 = (2 * tid) / G::ND;
   auto copy_cells = [&](int first_cell, double *dst) {
+    if constexpr (FASTFILL) {
+      if (nthr == 256 && (CT * G::ND) % 512 == 0) {
+        if constexpr (G::ND >= 512) {
+          for (int kc = 0; kc < CT; ++kc) {
+            const double *src = p.u + ((size_t)first_cell + kc * p.cstride) * G::ND + 2 * tid;
+            double *d0 = dst + kc * G::NDP + fbase;
+#pragma unroll
+            for (int m = 0; m < G::ND / 512; ++m) cp_async16(d0 + swz<D, N>(512 * m), src + 512 * m);
+          }
+        } else {
+          for (int j = 0; j < CT * G::ND / 512; ++j) {
+            const int kc = j * (512 / G::ND) + fcell0;
+            cp_async16(dst + kc * G::NDP + fbase, p.u + ((size_t)first_cell + kc * p.cstride) * G::ND + (2 * tid) % G::ND);
+          }
+        }
+        return;
+      }
+    }
     if constexpr (G::ND % 2 == 0) {
       for (int i = tid; i < ((CT * G::ND) >> 1); i += nthr) {
         const int e = 2 * i, kc = e / G::ND, x = e - kc * G::ND;
@@ -715,13 +748,13 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     // group g-1 done (its traces written, its epilogue finished); this group's cells and info are in smem
     __syncthreads();
     if (prev_unit >= 0 && tid == nthr - 1) st_release(p.flags + prev_unit, p.epoch | (prev_step + 1));
-    const CellInfo &ci = info0[s * CT + kk0];
+    const CellInfo &ci = info0[s * MAXCT + kk0];
     GroupBufs gb;
     gb.Ugrp = bufs + s * CND;
     gb.U = gb.Ugrp + (size_t)kk0 * G::NDP;
     gb.A = bufs + (s ^ 1) * CND + (size_t)kk0 * G::NDP;
-    gb.carry = carry0 + (size_t)(s * CT + kk0) * G::FN;
-    gb.carry_out = carry0 + (size_t)((s ^ 1) * CT + kk0) * G::FN;
+    gb.carry = carry0 + (size_t)(s * MAXCT + kk0) * G::FN;
+    gb.carry_out = carry0 + (size_t)((s ^ 1) * MAXCT + kk0) * G::FN;
     // cp.async groups of this thread, in commit order: the next group's records, this group's staged
     // traces per phase, then (last phase) RK dU and the next group's cells
     if (has_next) stage((long long)un * p.GPU + gn);
@@ -735,7 +768,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     }
     if (MODE == kModeRK && tid == 0 && p.prefetch)
       for (int kc = 0; kc < CT; ++kc)
-        prefetch_l2(p.du + ((size_t)info0[s * CT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
+        prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
     auto flags_next = [&]() {
       if (has_next) {
         cp_async_wait<NPH>();  // the records (the oldest group)
@@ -781,7 +814,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
         run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
       }
     }
-    if (has_next) resolve(info0 + (s ^ 1) * CT);
+    if (has_next) resolve(info0 + (s ^ 1) * MAXCT);
     cp_async_wait<0>();  // the next group's cells
     prev_unit = p.flags ? u : -1;
     prev_step = gi;

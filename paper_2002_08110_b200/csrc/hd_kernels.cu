@@ -233,10 +233,10 @@ CellGeometry geometry_dn(int L0, int L1, long long ncells, int pencil_ok) {
   using G = CGeo<D, N>;
   CellGeometry g{};
   g.phases = G::NPH;
-  const int maxCT = 256 / G::NT;
-  // two CTAs per SM when the group fits half the shared memory (HD_MINB = 2 in the launch bounds)
-  const int kSmemMax = HD_MINB > 1 ? 113 * 1024 : 227 * 1024;
-  auto smem_of = [&](int c) { return cell_smem_bytes<D, N>(c); };
+  // the kernel lays out max_ct cells (compile-time smem offsets); any group up to that size fits
+  const int maxCT = max_ct<D, N>();
+  const int kSmemMax = 227 * 1024;
+  auto smem_of = [&](int) { return cell_smem_bytes<D, N>(); };
   if (L0 <= maxCT && smem_of(L0) <= kSmemMax) {
     // multi-pencil groups: m whole pencils per group
     const long long npen = ncells / L0;
@@ -266,7 +266,7 @@ CellGeometry geometry_dn(int L0, int L1, long long ncells, int pencil_ok) {
     g.GPU = L0;
   }
   g.threads = ((g.CT * G::NT + 31) / 32) * 32;
-  g.smem = smem_of(g.CT);
+  g.smem = cell_smem_bytes<D, N>();
   return g;
 }
 
@@ -286,7 +286,7 @@ template <int D, int N, int MODE>
 cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) {
   // the host decided the geometry (hd_create_mesh); only the block size and smem follow from it
   const int threads = ((p.CT * CGeo<D, N>::NT + 31) / 32) * 32;
-  const int smem = cell_smem_bytes<D, N>(p.CT);
+  const int smem = cell_smem_bytes<D, N>();
   int grid = grid_max < p.nunits ? grid_max : p.nunits;
   if (grid < 1) return cudaSuccess;
   cell_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
