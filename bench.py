@@ -103,12 +103,29 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def host_cpu_meta():
+    """lscpu model, sockets, nproc and OMP_NUM_THREADS of the host the CPU oracle runs on (BASELINE.md plan)."""
+    meta = {"nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() == "Model name":
+                meta["cpu_model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                meta["sockets"] = v.strip()
+    except Exception:
+        pass
+    return meta
+
+
 def workload_config(name, spec, ndofs, nranks):
     return {"workload": name, "d_x": spec["d_x"], "d_v": spec["d_v"], "k": spec["k"], "cells": spec["cells"],
             "dofs": ndofs, "field": "vlasov-like" if any(any(r) for r in spec["a_lin"]) else "constant",
             "flux": "upwind", "basis": "Lagrange on Gauss points (collocation)",
-            "l2_policy": "inputs larger than L2 (%.1f GB per vector)" % (ndofs * 8 / 1e9),
-            "parallelism": f"x-slab x{nranks}" if nranks > 1 else "single GPU"}
+            "l2_policy": ("inputs larger than L2 (%.2f GB per vector)" % (ndofs * 8 / 1e9) if ndofs * 8 > 2 * 126e6 else
+                          "L2-resident inputs (%.3f GB per vector; --l2-flush for an HBM claim)" % (ndofs * 8 / 1e9)),
+            "parallelism": f"x-partition x{nranks}" if nranks > 1 else "single GPU"}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -172,9 +189,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * ndofs * 5 / (value * 1e9),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.config, spec, ndofs, 1),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             **host_cpu_meta()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": f"CPU oracle; ms_per_step extrapolated to the full workload; wall {wall:.1f} s"}
     print(json.dumps(line), flush=True)
@@ -200,7 +218,10 @@ def run_gpu(args):
     nccl_id = None
     if world > 1:
         nccl_id = _bcast_nccl_id(rank)
-    mesh = Mesh(spec, rank=rank, nranks=world, nccl_id=nccl_id)
+    xparts = None
+    if world > 1 and args.partition == "slabs":
+        xparts = [1] * (spec["d_x"] - 1) + [world]  # x-slabs of the slowest x dim (north star)
+    mesh = Mesh(spec, rank=rank, nranks=world, nccl_id=nccl_id, xparts=xparts)
     N = mesh.owned_dofs
     ndofs = configs.dof_count(spec)
     seed = configs.seed_of(args.config)
@@ -222,42 +243,71 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    flush_buf = None
+    if args.l2_flush:
+        # 2 x L2 of scratch written between timed repetitions (outside their events)
+        l2 = torch.cuda.get_device_properties(local).L2_cache_size
+        flush_buf = torch.empty(2 * l2 // 8, dtype=torch.float64, device="cuda")
+
+    def timed(fn, reps):
+        """Device time (ms) of reps calls of fn on the stream, CUDA events around each call; with --l2-flush
+        an L2 flush runs between the calls outside the events. Max over ranks."""
+        total = 0.0
+        if flush_buf is None:
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            barrier()
+            total = e0.elapsed_time(e1)
+        else:
+            for _ in range(reps):
+                flush_buf.fill_(1.0)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                barrier()
+                total += e0.elapsed_time(e1)
+        return max_over_ranks(total)
+
     # ---- warm-up (untimed)
     for _ in range(args.warmup):
         sol = mesh.rk_step(bufs, sol, 0.0, dt, 1, stream)
     barrier()
     # ---- timed region: exactly K steps, CUDA events on the launching stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
     l0 = mesh.launch_count
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        sol = mesh.rk_step(bufs, sol, 0.0, dt, 1, stream)
-    e1.record(stream)
-    barrier()
+    state = {"sol": sol}
+
+    def one_step():
+        state["sol"] = mesh.rk_step(bufs, state["sol"], 0.0, dt, 1, stream)
+
+    ms = timed(one_step, args.steps)
+    sol = state["sol"]
     clocks = sampler.stop()
     launches = mesh.launch_count - l0
-    ms = max_over_ranks(e0.elapsed_time(e1))
     ms_per_step = ms / args.steps
     value = ndofs * 5 * args.steps / (ms * 1e-3) / 1e9
     ok = bool(torch.isfinite(bufs[sol][:: max(1, N // 4096)]).all())
 
-    # roofline of the dominant kernel: the fused stage kernel is every launch of the step.
-    # Algorithmic bytes per launch: stage 1 reads U, writes dU and U' (24 B/DoF);
-    # stages 2..5 also read dU (32 B/DoF) -> (24 + 4*32)/5 = 30.4 B/DoF per launch on average.
+    # roofline of the dominant kernel: the fused stage kernel is every launch of the step (multi-rank: plus
+    # the halo pack). Algorithmic bytes per DoF (DESIGN.md "Roofline", SURVEY 8(d)): stage 1 reads U and
+    # writes dU and U' (24 B/DoF); stages 2..5 also read dU (32 B/DoF) -> 30.4 B/DoF per launch on average;
+    # the 32 B/DoF of SURVEY 8(d) is reported beside it. Whole-job bytes over the whole-job peak (N x HBM).
     peak, peak_kind = load_peak()
-    bytes_per_launch = N * 8 * (3 + 4 * 4) / 5.0
     launch_ms = ms_per_step / 5.0
-    achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
+    achieved = ndofs * 30.4 / (launch_ms * 1e-3) / 1e9
     traffic = load_traffic(args.config)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak * (1 if world == 1 else 1), "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "kernel": "cell_kernel<6,4,RK> (fused M^-1 A + LSRK stage)" if args.config == "6d" else
-                "cell_kernel (fused M^-1 A + LSRK stage)",
-                "algorithmic_bytes_per_dof": 30.4, "peak_kind": f"of {peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                "frac": achieved / (peak * world), "traffic": traffic,
+                "frac_32B": ndofs * 32.0 / (launch_ms * 1e-3) / 1e9 / (peak * world),
+                "kernel": f"cell_kernel<{spec['d_x'] + spec['d_v']},{spec['k'] + 1},RK> (fused M^-1 A + LSRK stage)",
+                "algorithmic_bytes_per_dof": 30.4,
+                "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs) x {world} GPU(s)"}
 
     # ---- the two operators of the metric name, timed alone (same workload, 16 B/DoF each)
     extra = {}
@@ -268,31 +318,29 @@ def run_gpu(args):
         for _ in range(2):
             mesh.apply_advection(u, v, 0.0, stream)
         barrier()
-        e0.record(stream)
-        for _ in range(reps):
-            mesh.apply_advection(u, v, 0.0, stream)
-        e1.record(stream)
-        barrier()
-        a_ms = max_over_ranks(e0.elapsed_time(e1)) / reps
+        a_ms = timed(lambda: mesh.apply_advection(u, v, 0.0, stream), reps) / reps
         w = bufs[(sol + 2) % 3]
         for _ in range(2):
             mesh.apply_inv_mass(w, stream)
         barrier()
-        e0.record(stream)
-        for _ in range(reps):
-            mesh.apply_inv_mass(w, stream)
-        e1.record(stream)
-        barrier()
-        m_ms = max_over_ranks(e0.elapsed_time(e1)) / reps
+        m_ms = timed(lambda: mesh.apply_inv_mass(w, stream), reps) / reps
         a_gdofs = ndofs / (a_ms * 1e-3) / 1e9
         m_gdofs = ndofs / (m_ms * 1e-3) / 1e9
+
+        def op_roofline(gdofs, kernel, key):
+            ach = gdofs * 16.0
+            return {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
+                    "frac": ach / (peak * world), "frac_of_8tbs": ach / (8000.0 * world),
+                    "traffic": load_traffic(args.config + "_" + key), "algorithmic_bytes_per_dof": 16.0,
+                    "kernel": kernel}
         extra = {
-            "apply_advection": {"gdofs": a_gdofs, "ms": a_ms, "hbm_frac_of_8tbs": a_gdofs * 16 / 8000 / world,
-                                "hbm_frac_of_measured": a_gdofs * 16 / peak / world},
-            "apply_inv_mass": {"gdofs": m_gdofs, "ms": m_ms, "hbm_frac_of_8tbs": m_gdofs * 16 / 8000 / world,
-                               "hbm_frac_of_measured": m_gdofs * 16 / peak / world},
-            "rk_stage": {"gdofs": value, "hbm_frac_of_8tbs": value * 32 / 8000 / world,
-                         "hbm_frac_of_measured_32B": value * 32 / peak / world},
+            "apply_advection": {"gdofs": a_gdofs, "ms": a_ms,
+                                "roofline": op_roofline(a_gdofs, "cell_kernel<..,A> (v <- A(u), weak form)", "adv")},
+            "apply_inv_mass": {"gdofs": m_gdofs, "ms": m_ms,
+                               "roofline": op_roofline(m_gdofs, "mass_kernel (u <- M^-1 u in place)", "mass")},
+            "rk_stage": {"gdofs": value, "hbm_frac_of_8tbs_32B": value * 32 / 8000 / world,
+                         "hbm_frac_of_measured_32B": value * 32 / peak / world,
+                         "hbm_frac_of_measured_30.4B": value * 30.4 / peak / world},
         }
         # keep the solution buffer intact for e2e: u, v, w are distinct
         mesh.fill_initial(bufs[0], cfg["recipe"], seed)
@@ -323,7 +371,7 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             v_c, cores, desc = cpu_oracle_sample(args.config, target_s=args.cpu_seconds)
-            cpu = {"value": v_c, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+            cpu = {"value": v_c, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc, **host_cpu_meta()}
         except Exception as ex:  # the oracle is test infrastructure; report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
 
@@ -331,7 +379,10 @@ def run_gpu(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": workload_config(args.config, spec, ndofs, world),
+                "config": dict(workload_config(args.config, spec, ndofs, world),
+                               l2_policy=("L2 flushed (2 x L2 scratch write) between timed repetitions"
+                                          if args.l2_flush else workload_config(args.config, spec, ndofs, world)["l2_policy"]),
+                               xparts=mesh.xparts[:spec["d_x"]]),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "finite": ok, **extra}
         print(json.dumps(line), flush=True)
@@ -365,7 +416,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ops", action="store_true")
+    ap.add_argument("--l2-flush", action="store_true", help="flush L2 between timed repetitions (3D/4D)")
+    ap.add_argument("--partition", default="auto", choices=["auto", "slabs"],
+                    help="multi-GPU x partition: smallest halo (auto) or x-slabs of the slowest x dim")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the line)
+        port = 29500 + (os.getpid() % 2000)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.warmup < 3 and args.impl == "gpu":
         print("warning: contract requires >= 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

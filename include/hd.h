@@ -22,7 +22,8 @@
  * j = sum_i m_i n^i (dim 0 = x_1 fastest ... last v dim slowest); owned cells in the order
  * [c_v][c_x - cx_begin], c_x and c_v lexicographic with the first axis fastest. With nranks = 1
  * this is the global order g = c_v |C_x| + c_x. Each cell occupies n^d consecutive
- * doubles; vectors must be 256-byte aligned device memory (cudaMalloc / torch allocations are).
+ * doubles; vectors must be 16-byte aligned device memory (HD_ERR_ARG otherwise; cudaMalloc and torch
+ * allocations are 256-byte aligned).
  *
  * Ownership: every DoF vector is caller-allocated device memory of hd_mesh_info's owned_dofs
  * doubles. The mesh owns its constant tables, halo plan and buffers, NCCL communicator and
@@ -100,6 +101,12 @@ hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream);
  * two buffers are scratch and are overwritten. */
 hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream);
 
+/* One fused stage s = 0..4 of the LSRK(5,4) step (the building block of hd_rk_step, exported for
+ * stage-by-stage checks): dU <- A_s dU + dt M^-1 A(U) (s = 0: dU <- dt M^-1 A(U), dU not read), then
+ * out <- U + B_s dU. U, dU, out: three distinct device vectors of owned_dofs doubles (HD_ERR_ARG if they
+ * overlap); U is not written. Multi-rank meshes exchange the halo of U first (NCCL transport). */
+hd_status hd_rk_stage(hd_mesh *m, const double *U, double *dU, double *out, int stage, double dt, void *stream);
+
 /* Multi-rank meshes WITHOUT an NCCL communicator (desc.nccl_id == NULL): all P ranks' meshes live in
  * this process on the current device and the halo is moved by device copies (loopback transport, the
  * same buffer layout NCCL delivers). ms[r] must be rank r of P. u, v: P device vectors;
@@ -128,7 +135,8 @@ hd_status hd_tables_1d(int n, double *xi, double *w, double *K, double *lam, dou
 hd_status hd_lsrk_coefficients(double *a, double *b);
 
 /* Upwind-trace plan of the mesh per dimension: tmode[i] = 0 (the cell
- * reads its upwind neighbour itself), 1 (ring of ring_slots[i] items in L2), 2 (full-size buffer). */
+ * reads its upwind neighbour itself or gets it from the same CTA), 1 (published into a ring of
+ * ring_slots[i] trace slots), 2 (published into a full-size buffer, one slot per cell). */
 hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots);
 
 /* 128-byte ncclUniqueId for hd_mesh_desc.nccl_id (rank 0 creates it and broadcasts it). Loads

@@ -34,7 +34,7 @@ _lib = None
 
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection",
-           "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_step_host", "hd_apply_advection_group",
+           "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_stage", "hd_rk_step_host", "hd_apply_advection_group",
            "hd_rk_step_group", "hd_fill_initial", "hd_tables_1d", "hd_lsrk_coefficients", "hd_mesh_traces",
            "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_launch_count", "hd_last_error"]
 
@@ -56,6 +56,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_apply_inv_mass.argtypes = [vp, vp, vp]
     lib.hd_apply_mass.argtypes = [vp, vp, vp]
     lib.hd_rk_step.argtypes = [vp, P(vp), P(ctypes.c_int), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
+    lib.hd_rk_stage.argtypes = [vp, vp, vp, vp, ctypes.c_int, ctypes.c_double, vp]
     lib.hd_rk_step_host.argtypes = [vp, vp, vp, P(vp), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
     lib.hd_fill_initial.argtypes = [vp, vp, ctypes.c_int, ctypes.c_ulonglong, vp]
     lib.hd_tables_1d.argtypes = [ctypes.c_int, dp, dp, dp, dp, dp]
@@ -196,6 +197,8 @@ class Mesh:
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
                 and x.numel() == self.owned_dofs):
             raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of {self.owned_dofs} elements")
+        if x.data_ptr() % 16:
+            raise ValueError(f"{name} must be 16-byte aligned (hd.h)")
         return ctypes.c_void_p(x.data_ptr())
 
     def apply_advection(self, u, v, t: float = 0.0, stream=None):
@@ -217,6 +220,11 @@ class Mesh:
         _check(load_library().hd_rk_step(self._h, arr, ctypes.byref(s), float(t), float(dt), int(nsteps),
                                          _stream_handle(stream)))
         return s.value
+
+    def rk_stage(self, U, dU, out, stage: int, dt: float, stream=None):
+        """One fused LSRK stage (0..4): dU <- A_s dU + dt M^-1 A(U); out <- U + B_s dU."""
+        _check(load_library().hd_rk_stage(self._h, self._vec(U, "U"), self._vec(dU, "dU"), self._vec(out, "out"),
+                                          int(stage), float(dt), _stream_handle(stream)))
 
     def rk_step_host(self, u_host, u_out_host, dbufs, t: float, dt: float, nsteps: int = 1, stream=None):
         import torch

@@ -195,6 +195,10 @@ void free_mesh(hd_mesh *m) {
   if (m->pack_dimsg) cudaFree(m->pack_dimsg);
   if (m->sendbuf) cudaFree(m->sendbuf);
   if (m->nccl_comm && g_nccl.ok) g_nccl.comm_destroy(m->nccl_comm);
+  for (int c = 0; c < hd::kMaxChunk; ++c)
+    if (m->ev_chunk[c]) cudaEventDestroy(m->ev_chunk[c]);
+  if (m->ev_u) cudaEventDestroy(m->ev_u);
+  if (m->comm) cudaStreamDestroy(m->comm);
   delete m;
 }
 
@@ -270,25 +274,86 @@ hd_status upload_schedule(hd_mesh *m) {
   return st;
 }
 
-// Halo plan and buffers of a multi-rank mesh (hd_plan.cpp).
+// Halo plan and buffers of a multi-rank mesh (hd_plan.cpp), cut into v-chunks: in pencil mode
+// the units are ordered with the slowest dim (a v dim, never split) outermost, so a range of its
+// traversal coordinate is a contiguous unit range, and -- the halo plane order also having that dim
+// slowest -- a contiguous range of every send list and receive buffer.
 hd_status setup_halo(hd_mesh *m) {
+  const int d = m->d;
   const long long fn = m->nd / m->n;
+  const long long Ls = m->pt.len[d - 1];
+  // chunks: ranges of the slowest dim's traversal coordinate t (reversed cell order when that dim follows
+  // a negative speed, as in the schedule)
+  m->nchunk = m->geo.pencil ? (int)std::min<long long>(4, Ls) : 1;
+  bool reversed = false;
+  if (m->geo.pencil && m->follow[d - 1]) {
+    long long cg[6];
+    for (int j = 0; j < d; ++j) cg[j] = m->pt.off[j];
+    reversed = hd::host_cell_sign(m->desc, m->h, d, d - 1, cg) != 0;
+  }
+  long long tcut[hd::kMaxChunk + 1];
+  for (int c = 0; c <= m->nchunk; ++c) tcut[c] = c * Ls / m->nchunk;
+  const long long units_per_slice = m->geo.pencil ? m->nunits / Ls : 0;
+  for (int c = 0; c <= m->nchunk; ++c) m->chunk_u[c] = m->geo.pencil ? (int)(tcut[c] * units_per_slice) : (c ? m->nunits : 0);
+  // cell range [c0, c1) of the slowest coordinate of chunk c
+  auto crange = [&](int c, long long &c0, long long &c1) {
+    if (!m->geo.pencil) {
+      c0 = 0;
+      c1 = Ls;
+    } else if (reversed) {
+      c0 = Ls - tcut[c + 1];
+      c1 = Ls - tcut[c];
+    } else {
+      c0 = tcut[c];
+      c1 = tcut[c + 1];
+    }
+  };
   std::vector<int> cells, dimsg;
   for (int i = 0; i < m->desc.d_x; ++i) {
     hd::HaloDim &hd = m->halo[i];
     hd::make_halo(m->desc, m->pt, m->h, i, hd);
+  }
+  for (int c = 0; c < m->nchunk; ++c) {
+    hd_mesh::ChunkHalo &ch = m->chunk[c];
+    std::memset(&ch, 0, sizeof(ch));
+    ch.pe0 = (long long)cells.size();
+    long long c0, c1;
+    crange(c, c0, c1);
+    for (int i = 0; i < m->desc.d_x; ++i) {
+      const hd::HaloDim &hd = m->halo[i];
+      if (!hd.active) continue;
+      // plane positions of the chunk: [j0, j1) (the slowest dim is slowest in the plane order too)
+      const long long plane = (long long)hd.slot.size(), per = plane / Ls;
+      const long long j0 = c0 * per, j1 = c1 * per;
+      long long before0 = 0, before1 = 0, in0 = 0, in1 = 0;  // sign-0 / sign-1 positions before / in [j0, j1)
+      for (long long j = 0; j < j1; ++j) {
+        const bool s1 = hd.slot[j] >= hd.n_from_left;
+        if (j < j0) (s1 ? before1 : before0) += 1;
+        else (s1 ? in1 : in0) += 1;
+      }
+      // to the right rank: my high-face cells with a_i > 0 (sign 0), in plane order; to the left: sign 1
+      ch.sr[i][0] = (long long)cells.size();
+      ch.sr[i][1] = in0;
+      for (long long q = before0; q < before0 + in0; ++q) {
+        cells.push_back(hd.send_right[q]);
+        dimsg.push_back(i);
+      }
+      ch.sl[i][0] = (long long)cells.size();
+      ch.sl[i][1] = in1;
+      for (long long q = before1; q < before1 + in1; ++q) {
+        cells.push_back(hd.send_left[q]);
+        dimsg.push_back(i | (1 << 8));
+      }
+      ch.rl[i][0] = before0;
+      ch.rl[i][1] = in0;
+      ch.rr[i][0] = hd.n_from_left + before1;
+      ch.rr[i][1] = in1;
+    }
+    ch.pe1 = (long long)cells.size();
+  }
+  for (int i = 0; i < m->desc.d_x; ++i) {
+    const hd::HaloDim &hd = m->halo[i];
     if (!hd.active) continue;
-    // send buffer per dim: [to the right rank (a_i > 0, tau of the right face)][to the left rank]
-    m->send_off_right[i] = (long long)cells.size();
-    for (int c : hd.send_right) {
-      cells.push_back(c);
-      dimsg.push_back(i);
-    }
-    m->send_off_left[i] = (long long)cells.size();
-    for (int c : hd.send_left) {
-      cells.push_back(c);
-      dimsg.push_back(i | (1 << 8));
-    }
     hd_status st = upload(&m->hslot[i], hd.slot.data(), hd.slot.size(), "halo slot table");
     if (st != HD_OK) return st;
     st = upload(&m->hbuf[i], (const double *)nullptr, (size_t)(hd.n_from_left + hd.n_from_right) * fn,
@@ -302,37 +367,42 @@ hd_status setup_halo(hd_mesh *m) {
   return st;
 }
 
-// Pack the outgoing traces of u (every stage: the operator input changes) with the launch's speeds.
-hd_status halo_pack(hd_mesh *m, const hd::CellParams &p, const double *u, cudaStream_t s) {
-  if (m->nsend == 0) return HD_OK;
+// Pack the outgoing traces of chunk c of u (every stage: the operator input changes) with the launch's
+// speeds, into the chunk's part of the send buffer.
+hd_status halo_pack(hd_mesh *m, const hd::CellParams &p, const double *u, int c, cudaStream_t s) {
+  const hd_mesh::ChunkHalo &ch = m->chunk[c];
+  if (ch.pe1 == ch.pe0) return HD_OK;
+  const long long fn = m->nd / m->n;
   hd::PackParams pp;
   pp.u = u;
-  pp.out = m->sendbuf;
-  pp.cells = m->pack_cells;
-  pp.dimsg = m->pack_dimsg;
-  pp.nent = m->nsend;
+  pp.out = m->sendbuf + ch.pe0 * fn;
+  pp.cells = m->pack_cells + ch.pe0;
+  pp.dimsg = m->pack_dimsg + ch.pe0;
+  pp.nent = ch.pe1 - ch.pe0;
   cudaError_t e = hd::launch_pack_kernel(m->d, m->n, pp, p, s, &m->launches);
   if (e != cudaSuccess) return cuda_fail(e, "halo pack kernel");
   return HD_OK;
 }
 
-// NCCL transport: one group per exchange; per peer the order is canonical on both sides (dims
-// ascending; per dim: send to the right before send to the left, receive from the left before receive
-// from the right), so every send meets its receive even when left == right (two ranks along a dim).
-hd_status halo_exchange_nccl(hd_mesh *m, cudaStream_t s) {
+// NCCL transport, chunk c: one group; per peer the order is canonical on both sides (dims ascending; per
+// dim: send to the right before send to the left, receive from the left before receive from the right),
+// so every send meets its receive even when left == right (two ranks along a dim). Both sides compute the
+// same counts (v is never split), so the zero-count skips agree.
+hd_status halo_exchange_nccl(hd_mesh *m, int c, cudaStream_t s) {
   const long long fn = m->nd / m->n;
+  const hd_mesh::ChunkHalo &ch = m->chunk[c];
   nccl_result r = g_nccl.group_start();
   if (r) return nccl_fail(r, "ncclGroupStart");
   for (int i = 0; i < m->desc.d_x; ++i) {
     const hd::HaloDim &hd = m->halo[i];
     if (!hd.active) continue;
-    const size_t nr = hd.send_right.size() * fn, nl = hd.send_left.size() * fn;
-    if (nr) r = g_nccl.send(m->sendbuf + m->send_off_right[i] * fn, nr, kNcclFloat64, hd.right, m->nccl_comm, s);
-    if (!r && nl) r = g_nccl.send(m->sendbuf + m->send_off_left[i] * fn, nl, kNcclFloat64, hd.left, m->nccl_comm, s);
-    if (!r && hd.n_from_left)
-      r = g_nccl.recv(m->hbuf[i], hd.n_from_left * fn, kNcclFloat64, hd.left, m->nccl_comm, s);
-    if (!r && hd.n_from_right)
-      r = g_nccl.recv(m->hbuf[i] + hd.n_from_left * fn, hd.n_from_right * fn, kNcclFloat64, hd.right, m->nccl_comm, s);
+    if (ch.sr[i][1]) r = g_nccl.send(m->sendbuf + ch.sr[i][0] * fn, ch.sr[i][1] * fn, kNcclFloat64, hd.right, m->nccl_comm, s);
+    if (!r && ch.sl[i][1])
+      r = g_nccl.send(m->sendbuf + ch.sl[i][0] * fn, ch.sl[i][1] * fn, kNcclFloat64, hd.left, m->nccl_comm, s);
+    if (!r && ch.rl[i][1])
+      r = g_nccl.recv(m->hbuf[i] + ch.rl[i][0] * fn, ch.rl[i][1] * fn, kNcclFloat64, hd.left, m->nccl_comm, s);
+    if (!r && ch.rr[i][1])
+      r = g_nccl.recv(m->hbuf[i] + ch.rr[i][0] * fn, ch.rr[i][1] * fn, kNcclFloat64, hd.right, m->nccl_comm, s);
     if (r) {
       g_nccl.group_end();
       return nccl_fail(r, "ncclSend/ncclRecv");
@@ -343,23 +413,24 @@ hd_status halo_exchange_nccl(hd_mesh *m, cudaStream_t s) {
   return HD_OK;
 }
 
-// Loopback transport (all ranks' meshes in this process on one device): device copies from each
-// neighbour's send buffer into the receive buffer, in the same layout NCCL would deliver.
-hd_status halo_exchange_loopback(hd_mesh **ms, int P, cudaStream_t s) {
+// Loopback transport, chunk c (all ranks' meshes in this process on one device): device copies from each
+// neighbour's send buffer into the receive buffer, in the layout NCCL would deliver.
+hd_status halo_exchange_loopback(hd_mesh **ms, int P, int c, cudaStream_t s) {
   for (int r = 0; r < P; ++r) {
     hd_mesh *m = ms[r];
     const long long fn = m->nd / m->n;
+    const hd_mesh::ChunkHalo &ch = m->chunk[c];
     for (int i = 0; i < m->desc.d_x; ++i) {
       const hd::HaloDim &hd = m->halo[i];
       if (!hd.active) continue;
       const hd_mesh *L = ms[hd.left], *R = ms[hd.right];
       cudaError_t e = cudaSuccess;
-      if (hd.n_from_left)
-        e = cudaMemcpyAsync(m->hbuf[i], L->sendbuf + L->send_off_right[i] * fn, hd.n_from_left * fn * sizeof(double),
-                            cudaMemcpyDeviceToDevice, s);
-      if (e == cudaSuccess && hd.n_from_right)
-        e = cudaMemcpyAsync(m->hbuf[i] + hd.n_from_left * fn, R->sendbuf + R->send_off_left[i] * fn,
-                            hd.n_from_right * fn * sizeof(double), cudaMemcpyDeviceToDevice, s);
+      if (ch.rl[i][1])
+        e = cudaMemcpyAsync(m->hbuf[i] + ch.rl[i][0] * fn, L->sendbuf + L->chunk[c].sr[i][0] * fn,
+                            ch.rl[i][1] * fn * sizeof(double), cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess && ch.rr[i][1])
+        e = cudaMemcpyAsync(m->hbuf[i] + ch.rr[i][0] * fn, R->sendbuf + R->chunk[c].sl[i][0] * fn,
+                            ch.rr[i][1] * fn * sizeof(double), cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return cuda_fail(e, "loopback halo copy");
     }
   }
@@ -509,7 +580,18 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     return cuda_fail(e, "cell kernel occupancy");
   }
   st = plan_traces(m);
+  m->nchunk = 1;
+  m->chunk_u[0] = 0;
+  m->chunk_u[1] = m->nunits;
+  std::memset(m->chunk, 0, sizeof(m->chunk));
   if (st == HD_OK && desc->nranks > 1) st = setup_halo(m);
+  if (st == HD_OK && desc->nranks > 1 && desc->nccl_id) {
+    cudaError_t e2 = cudaStreamCreateWithFlags(&m->comm, cudaStreamNonBlocking);
+    if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&m->ev_u, cudaEventDisableTiming);
+    for (int c = 0; c < m->nchunk && e2 == cudaSuccess; ++c)
+      e2 = cudaEventCreateWithFlags(&m->ev_chunk[c], cudaEventDisableTiming);
+    if (e2 != cudaSuccess) st = cuda_fail(e2, "halo stream / events");
+  }
   if (st == HD_OK) st = upload_schedule(m);
   if (st == HD_OK && desc->nranks > 1 && desc->nccl_id) {
     st = load_nccl();
@@ -719,25 +801,77 @@ hd_status hd_halo_list(const hd_mesh_desc *desc, int dim, int which, long long *
 
 namespace {
 
-// One fused cell-kernel launch over U (A mode or an RK stage). For nranks > 1 the halo traces of U are
-// packed and exchanged first (NCCL transport), unless the caller did it (loopback group driver).
-hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
-                       double b, cudaStream_t s, bool exchange) {
+// Launch-dependent kernel parameters of one stage (A mode or an RK stage) and its epoch; every kernel
+// launch of the stage (one, or one per v-chunk) shares the epoch, so traces published by an earlier
+// chunk's launch are recognised by the later ones.
+hd_status begin_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
+                      double b, cudaStream_t s) {
   hd_status st = next_epoch(m, p, s);
   if (st != HD_OK) return st;
-  if (exchange && m->desc.nranks > 1) {
-    st = halo_pack(m, p, U, s);
-    if (st == HD_OK) st = halo_exchange_nccl(m, s);
-    if (st != HD_OK) return st;
-  }
   p.u = U;
   p.du = dU;
   p.out = out;
   p.mode = mode;
   p.rk_a = a;
   p.rk_b = b;
+  return HD_OK;
+}
+hd_status launch_units(hd_mesh *m, hd::CellParams &p, int u0, int u1, cudaStream_t s) {
+  p.u_begin = u0;
+  p.u_end = u1;
   cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, s, &m->launches, m->grid);
   if (e != cudaSuccess) return cuda_fail(e, "cell kernel");
+  return HD_OK;
+}
+
+// One stage of a mesh with its own transport: one launch over all units (one rank), or for nranks > 1
+// (NCCL) the v-chunk pipeline: on the mesh's comm stream, after U is ready, chunk c's
+// outgoing traces are packed and exchanged (one NCCL group per chunk); on s, chunk c's units run as soon as
+// chunk c's traces have arrived -- so the exchange of chunk c+1 overlaps the cell kernel of chunk c.
+hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
+                       double b, cudaStream_t s) {
+  hd_status st = begin_stage(m, p, U, dU, out, mode, a, b, s);
+  if (st != HD_OK) return st;
+  if (m->desc.nranks == 1) return launch_units(m, p, 0, m->nunits, s);
+  cudaError_t e = cudaEventRecord(m->ev_u, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(m->comm, m->ev_u, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "halo stream order");
+  for (int c = 0; c < m->nchunk; ++c) {
+    st = halo_pack(m, p, U, c, m->comm);
+    if (st == HD_OK) st = halo_exchange_nccl(m, c, m->comm);
+    if (st != HD_OK) return st;
+    e = cudaEventRecord(m->ev_chunk[c], m->comm);
+    if (e != cudaSuccess) return cuda_fail(e, "halo event");
+  }
+  for (int c = 0; c < m->nchunk; ++c) {
+    e = cudaStreamWaitEvent(s, m->ev_chunk[c], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "halo event wait");
+    st = launch_units(m, p, m->chunk_u[c], m->chunk_u[c + 1], s);
+    if (st != HD_OK) return st;
+  }
+  return HD_OK;
+}
+
+// One stage of P in-process ranks (loopback transport), chunk by chunk: pack chunk c of every rank, copy
+// it, run chunk c of every rank -- the same chunk plan, buffers and epochs as the NCCL pipeline, serialised.
+hd_status launch_stage_group(hd_mesh **ms, int P, std::vector<hd::CellParams> &ps, const double *const *U,
+                             double *const *dU, double *const *out, int mode, double a, double b, cudaStream_t s) {
+  for (int r = 0; r < P; ++r) {
+    hd_status st = begin_stage(ms[r], ps[r], U[r], dU ? dU[r] : nullptr, out[r], mode, a, b, s);
+    if (st != HD_OK) return st;
+  }
+  for (int c = 0; c < ms[0]->nchunk; ++c) {
+    for (int r = 0; r < P; ++r) {
+      hd_status st = halo_pack(ms[r], ps[r], U[r], c, s);
+      if (st != HD_OK) return st;
+    }
+    hd_status st = halo_exchange_loopback(ms, P, c, s);
+    if (st != HD_OK) return st;
+    for (int r = 0; r < P; ++r) {
+      st = launch_units(ms[r], ps[r], ms[r]->chunk_u[c], ms[r]->chunk_u[c + 1], s);
+      if (st != HD_OK) return st;
+    }
+  }
   return HD_OK;
 }
 
@@ -786,7 +920,7 @@ hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, v
   hd::CellParams p;
   fill_cell_params(m, p);
   set_dtfac(m, p, 1.0);
-  return launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream, true);
+  return launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream);
 }
 
 hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {
@@ -803,13 +937,29 @@ hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, 
   for (int step = 0; step < nsteps; ++step) {
     for (int s = 0; s < 5; ++s) {
       st = launch_stage(m, p, buf[iu], buf[idu], buf[iw], s == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[s], kRkB[s],
-                        (cudaStream_t)stream, true);
+                        (cudaStream_t)stream);
       if (st != HD_OK) return st;
       std::swap(iu, iw);
     }
   }
   *sol = iu;
   return HD_OK;
+}
+
+hd_status hd_rk_stage(hd_mesh *m, const double *U, double *dU, double *out, int stage, double dt, void *stream) {
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  if (stage < 0 || stage > 4) return fail(HD_ERR_ARG, "stage must be 0..4");
+  double *bufs[3] = {const_cast<double *>(U), dU, out};
+  int sol = 0;
+  hd_status st = check_bufs(m, bufs, &sol, 1, dt);
+  if (st == HD_OK) st = check_transport(m);
+  if (st == HD_OK) st = ensure_tables(m);
+  if (st != HD_OK) return st;
+  hd::CellParams p;
+  fill_cell_params(m, p);
+  set_dtfac(m, p, dt);
+  return launch_stage(m, p, U, dU, out, stage == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[stage], kRkB[stage],
+                      (cudaStream_t)stream);
 }
 
 hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double **v, double t, void *stream) {
@@ -826,16 +976,8 @@ hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double
   for (int r = 0; r < P; ++r) {
     fill_cell_params(ms[r], ps[r]);
     set_dtfac(ms[r], ps[r], 1.0);
-    hd_status st = halo_pack(ms[r], ps[r], u[r], s);
-    if (st != HD_OK) return st;
   }
-  hd_status st = halo_exchange_loopback(ms, P, s);
-  if (st != HD_OK) return st;
-  for (int r = 0; r < P; ++r) {
-    st = launch_stage(ms[r], ps[r], u[r], nullptr, v[r], hd::kModeAdvection, 0.0, 0.0, s, false);
-    if (st != HD_OK) return st;
-  }
-  return HD_OK;
+  return launch_stage_group(ms, P, ps, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, s);
 }
 
 hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double t, double dt, int nsteps,
@@ -856,19 +998,17 @@ hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double 
     set_dtfac(ms[r], ps[r], dt);
   }
   int iu = *sol, idu = (*sol + 1) % 3, iw = (*sol + 2) % 3;
+  std::vector<double *> U(P), DU(P), W(P);
   for (int step = 0; step < nsteps; ++step) {
     for (int st5 = 0; st5 < 5; ++st5) {
       for (int r = 0; r < P; ++r) {
-        hd_status st = halo_pack(ms[r], ps[r], bufs[3 * r + iu], s);
-        if (st != HD_OK) return st;
+        U[r] = bufs[3 * r + iu];
+        DU[r] = bufs[3 * r + idu];
+        W[r] = bufs[3 * r + iw];
       }
-      hd_status st = halo_exchange_loopback(ms, P, s);
+      hd_status st = launch_stage_group(ms, P, ps, U.data(), DU.data(), W.data(),
+                                        st5 == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[st5], kRkB[st5], s);
       if (st != HD_OK) return st;
-      for (int r = 0; r < P; ++r) {
-        st = launch_stage(ms[r], ps[r], bufs[3 * r + iu], bufs[3 * r + idu], bufs[3 * r + iw],
-                          st5 == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[st5], kRkB[st5], s, false);
-        if (st != HD_OK) return st;
-      }
       std::swap(iu, iw);
     }
   }

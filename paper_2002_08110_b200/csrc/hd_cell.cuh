@@ -601,7 +601,8 @@ __host__ __device__ constexpr int cell_smem_bytes() {
   return SmemMap<D, N>(max_ct<D, N>()).bytes;
 }
 
-// Persistent kernel: CTA b processes units b, b + grid, ... in increasing order; each unit is GPU groups.
+// Persistent kernel: CTA b processes units u_begin + b, + grid, ... < u_end in increasing order (the whole
+// mesh, or one v-chunk of a pipelined multi-rank stage); each unit is GPU groups.
 // Per group: the next group's schedule records are staged (cp.async) at the start, its producers' flags
 // read (ld.acquire) one phase later and resolved after the epilogue; its cells stream into the free buffer
 // during the last phase. The progress flag of a group is released (st.release after a CTA barrier) at
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   const int r = tid - k * G::NT;
   const bool active = k < CT;
   const int kk0 = active ? k : 0;
-  if ((int)blockIdx.x >= p.nunits) return;
+  if (p.u_begin + (int)blockIdx.x >= p.u_end) return;
   phase_table<D, N, MODE>(p, r, ptab);  // read only by this thread
   const int nitems = CT * D;
 
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     }
   };
 
-  int u = blockIdx.x, gi = 0, it = 0;
+  int u = p.u_begin + (int)blockIdx.x, gi = 0, it = 0;
   // prologue: group 0's schedule and cells
   stage((long long)u * p.GPU);
   cp_async_wait<0>();
@@ -737,14 +738,14 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   cp_async_commit();
   cp_async_wait<0>();
   int prev_unit = -1, prev_step = 0;
-  while (u < p.nunits) {
+  while (u < p.u_end) {
     const int s = it & 1;
     int un = u, gn = gi + 1;
     if (gn >= p.GPU) {
       un = u + gridDim.x;
       gn = 0;
     }
-    const bool has_next = un < p.nunits;
+    const bool has_next = un < p.u_end;
     // group g-1 done (its traces written, its epilogue finished); this group's cells and info are in smem
     __syncthreads();
     if (prev_unit >= 0 && tid == nthr - 1) st_release(p.flags + prev_unit, p.epoch | (prev_step + 1));

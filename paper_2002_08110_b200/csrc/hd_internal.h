@@ -12,6 +12,7 @@ namespace hd {
 
 constexpr int kMaxD = 6;
 constexpr int kMaxN = 6;
+constexpr int kMaxChunk = 8;  // v-chunks of a pipelined multi-rank stage
 
 // 1D tables for n nodes: everything the cell kernel needs from the
 // reference interval. Computed on the host in long double (hd_tables.cpp).
@@ -91,7 +92,8 @@ struct CellParams {
   double rk_a, rk_b;      // stage coefficients A_s, B_s
   double dtfac;           // 1 (A-mode) or dt (RK-mode): folded into the line speeds
   double jdet;            // |J| = prod h_i
-  int nunits;             // units of this launch
+  int nunits;             // units of the mesh
+  int u_begin, u_end;     // units of this launch (all, or one v-chunk of a pipelined multi-rank stage)
   int CT;                 // cells per group
   int GPU;                // groups (steps) per unit
   int ND;                 // n^d: doubles per cell
@@ -201,8 +203,19 @@ struct hd_mesh {
   hd::HaloDim halo[3];
   double *hbuf[3];
   int *hslot[3];
-  long long send_off_right[3], send_off_left[3];  // entry offsets into the send buffer
-  long long nsend;                                // entries
+  long long nsend;                                // entries of the send list (chunk-major)
+  // v-chunk pipeline of a multi-rank stage: chunk c = the units [chunk_u[c], chunk_u[c+1]),
+  // i.e. the cells whose slowest (v) coordinate lies in one range. Per chunk: its send-list entries
+  // [pe0, pe1) and, per x dim, (offset, count) of the traces sent to the right / left rank (entries of the
+  // send list) and received from the left / right rank (slots of hbuf[i]).
+  int nchunk;
+  int chunk_u[hd::kMaxChunk + 1];
+  struct ChunkHalo {
+    long long pe0, pe1;
+    long long sr[3][2], sl[3][2], rl[3][2], rr[3][2];
+  } chunk[hd::kMaxChunk];
+  cudaStream_t comm;                              // NCCL transport: pack + exchange stream
+  cudaEvent_t ev_u, ev_chunk[hd::kMaxChunk];
   int *pack_cells, *pack_dimsg;
   double *sendbuf;
   void *nccl_comm;         // ncclComm_t when the NCCL transport is used

@@ -287,7 +287,8 @@ cudaError_t launch_cell_impl(const CellParams &p, cudaStream_t s, int grid_max) 
   // the host decided the geometry (hd_create_mesh); only the block size and smem follow from it
   const int threads = ((p.CT * CGeo<D, N>::NT + 31) / 32) * 32;
   const int smem = cell_smem_bytes<D, N>();
-  int grid = grid_max < p.nunits ? grid_max : p.nunits;
+  const int nu = p.u_end - p.u_begin;
+  int grid = grid_max < nu ? grid_max : nu;
   if (grid < 1) return cudaSuccess;
   cell_kernel<D, N, MODE><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError();

@@ -169,7 +169,10 @@ def test_config_full_parity(name):
     assert_close(host(bufs[sol]), ref, TOL_RK10, name + " rk10")
 
 
-def test_config_5d_full_apply_and_reduced_rk10():
+def test_config_5d_full_apply_and_rk10():
+    """Full-size 5D (255M DoFs, the bench's 5D launch configuration: pencil units of CT = 4 cells): one
+    apply_advection and 10 LSRK steps against the oracle on the whole vector (north star: <= 1e-12 per
+    application, <= 1e-10 after 10 steps; the oracle RK10 takes a few minutes on the host cores)."""
     torch = _torch()
     cfg = configs.CONFIGS["5d"]
     spec = cfg["spec"]
@@ -186,16 +189,13 @@ def test_config_5d_full_apply_and_reduced_rk10():
     g = torch.empty_like(ud)
     m.fill_initial(g, cfg["recipe"], seed)
     assert_close(host(g), u, 1e-14, "5d fill")
-    del ud, g
-    # 10 RK steps on the same field and degree, fewer cells (v = 0 stays a cell boundary)
-    red = dict(spec, cells=[6, 6, 6, 4, 4])
-    ur = inputs.full_vector(red, cfg["recipe"], seed)
-    mr = mesh(red)
+    del g, got
     dt = configs.time_step(spec, cfg["cfl"])
-    bufs = [dev(ur), torch.empty(ur.size, dtype=torch.float64, device="cuda"),
-            torch.empty(ur.size, dtype=torch.float64, device="cuda")]
-    sol = mr.rk_step(bufs, 0, 0.0, dt, nsteps=10)
-    assert_close(host(bufs[sol]), oracle.rk_steps(red, ur, 0.0, dt, 10), TOL_RK10, "5d reduced rk10")
+    bufs = [ud, torch.empty_like(ud), torch.empty_like(ud)]
+    sol = m.rk_step(bufs, 0, 0.0, dt, nsteps=10)
+    got = host(bufs[sol])
+    del bufs, ud
+    assert_close(got, oracle.rk_steps(spec, u, 0.0, dt, 10), TOL_RK10, "5d rk10")
 
 
 def _sampled_cells(spec, count, rng):
@@ -253,6 +253,46 @@ def test_config_6d_sampled_parity():
                a_const=[0.0] * 6)
     ref_im = np.stack([oracle.apply_inv_mass(one, own[i]) for i in range(len(ids))])
     assert_close(host(u.view(-1, nd)[idx]), ref_im, 1e-14, "6d sampled M^-1")
+
+
+def _gather_cells(vec, nd, ids):
+    torch = _torch()
+    return host(vec.view(-1, nd)[torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64)).cuda()])
+
+
+def test_config_6d_rk_stages_sampled_parity():
+    """Full-size 6D RK stages in the bench's launch configuration (cell_kernel<6,4,RK>, 10^6 cells, pencil
+    units, skew 2, published traces, direct-read fallbacks): every one of the 5 stages of a step is run
+    through hd_rk_stage and, on >= 1024 random cells plus boundary cells, compared with the oracle's merged
+    operator of the sampled cells (given U and its neighbours) followed by the 2N update."""
+    torch = _torch()
+    cfg = configs.CONFIGS["6d"]
+    spec = cfg["spec"]
+    m = mesh(spec)
+    N = m.owned_dofs
+    nd = 4 ** 6
+    dt = configs.time_step(spec, cfg["cfl"])
+    A, B, _ = oracle.rk_coefficients()
+    bufs = [torch.empty(N, dtype=torch.float64, device="cuda") for _ in range(3)]
+    m.fill_initial(bufs[0], cfg["recipe"], configs.seed_of("6d"))
+    iu, idu, iw = 0, 1, 2
+    rng = np.random.default_rng(606)
+    for s in range(5):
+        ids = _sampled_cells(spec, 1024, rng)
+        nb = inputs.neighbour_ids(spec, ids)
+        U = bufs[iu]
+        own = _gather_cells(U, nd, ids)
+        nbv = _gather_cells(U, nd, nb.reshape(-1)).reshape(len(ids), -1, nd)
+        du_in = _gather_cells(bufs[idu], nd, ids) if s > 0 else np.zeros_like(own)
+        m.rk_stage(U, bufs[idu], bufs[iw], s, dt)
+        got_du = _gather_cells(bufs[idu], nd, ids)
+        got_u = _gather_cells(bufs[iw], nd, ids)
+        r = oracle.apply_advection_cells(spec, ids, np.concatenate([own[:, None, :], nbv], axis=1), merged=True)
+        ref_du = A[s] * du_in + dt * r
+        ref_u = own + B[s] * ref_du
+        assert_close(got_du, ref_du, TOL_APPLY, f"6d stage {s} dU")
+        assert_close(got_u, ref_u, TOL_APPLY, f"6d stage {s} U")
+        iu, iw = iw, iu
 
 
 def test_6d_full_rk_step_conserves_mass():
