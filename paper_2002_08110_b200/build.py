@@ -57,6 +57,36 @@ def build(force: bool = False, verbose_ptxas: bool = False, out: str = LIB, defi
     return out
 
 
+def build_all(force: bool = False) -> None:
+    """The product library and its HD_DEBUG twin (device-side checks, bench configs only; tests use it),
+    compiled concurrently."""
+    import threading
+    dbg = os.path.join(HERE, "libhd_debug.so")
+    errs = []
+
+    def run_debug():
+        try:
+            if force or not os.path.exists(dbg) or needs_build_of(dbg):
+                build(force=True, out=dbg, defines=("HD_DEBUG", "HD_ONLY_BENCH"))
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+    t = threading.Thread(target=run_debug)
+    t.start()
+    build(force=force)
+    t.join()
+    if errs:
+        raise errs[0]
+
+
+def needs_build_of(path: str) -> bool:
+    t = os.path.getmtime(path)
+    for f in SOURCES + HEADERS + ["../build.py"]:
+        p = os.path.normpath(os.path.join(CSRC, f))
+        if os.path.exists(p) and os.path.getmtime(p) > t:
+            return True
+    return False
+
+
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]

@@ -46,6 +46,7 @@ typedef struct {
 } nccl_unique_id;
 typedef int nccl_result;
 constexpr int kNcclFloat64 = 8;
+constexpr int kNcclInt32 = 2;
 
 }  // namespace
 
@@ -125,6 +126,11 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.schedc = m->schedc;
   p.flags = m->flags;
   p.dtfac = 1.0;
+  p.err = m->dbg;
+  p.stag = m->dbg + 1;
+  p.rtag = m->dbg + 7;
+  p.ncells = m->ncells_local;
+  for (int i = 0; i < 3; ++i) p.nhalo[i] = m->halo[i].n_from_left + m->halo[i].n_from_right;
   for (int i = 0; i < d; ++i) {
     p.L[i] = (int)m->pt.len[i];
     p.coff[i] = (int)m->pt.off[i];
@@ -186,6 +192,7 @@ void free_mesh(hd_mesh *m) {
     if (m->tbuf[i]) cudaFree(m->tbuf[i]);
   if (m->flags) cudaFree(m->flags);
   if (m->sched) cudaFree(m->sched);
+  if (m->dbg) cudaFree(m->dbg);
   if (m->schedc) cudaFree(m->schedc);
   for (int i = 0; i < 3; ++i) {
     if (m->hbuf[i]) cudaFree(m->hbuf[i]);
@@ -403,6 +410,13 @@ hd_status halo_exchange_nccl(hd_mesh *m, int c, cudaStream_t s) {
       r = g_nccl.recv(m->hbuf[i] + ch.rl[i][0] * fn, ch.rl[i][1] * fn, kNcclFloat64, hd.left, m->nccl_comm, s);
     if (!r && ch.rr[i][1])
       r = g_nccl.recv(m->hbuf[i] + ch.rr[i][0] * fn, ch.rr[i][1] * fn, kNcclFloat64, hd.right, m->nccl_comm, s);
+#ifdef HD_DEBUG
+    // freshness tags travel with the traces; every rank runs the same build
+    if (!r) r = g_nccl.send(m->dbg + 1 + i * 2, 1, kNcclInt32, hd.right, m->nccl_comm, s);
+    if (!r) r = g_nccl.send(m->dbg + 2 + i * 2, 1, kNcclInt32, hd.left, m->nccl_comm, s);
+    if (!r) r = g_nccl.recv(m->dbg + 7 + i * 2, 1, kNcclInt32, hd.left, m->nccl_comm, s);
+    if (!r) r = g_nccl.recv(m->dbg + 8 + i * 2, 1, kNcclInt32, hd.right, m->nccl_comm, s);
+#endif
     if (r) {
       g_nccl.group_end();
       return nccl_fail(r, "ncclSend/ncclRecv");
@@ -431,6 +445,12 @@ hd_status halo_exchange_loopback(hd_mesh **ms, int P, int c, cudaStream_t s) {
       if (e == cudaSuccess && ch.rr[i][1])
         e = cudaMemcpyAsync(m->hbuf[i] + ch.rr[i][0] * fn, R->sendbuf + R->chunk[c].sl[i][0] * fn,
                             ch.rr[i][1] * fn * sizeof(double), cudaMemcpyDeviceToDevice, s);
+#ifdef HD_DEBUG
+      // freshness tags travel with the traces
+      if (e == cudaSuccess) e = cudaMemcpyAsync(m->dbg + 7 + i * 2, L->dbg + 1 + i * 2, sizeof(int), cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(m->dbg + 8 + i * 2, R->dbg + 2 + i * 2, sizeof(int), cudaMemcpyDeviceToDevice, s);
+#endif
       if (e != cudaSuccess) return cuda_fail(e, "loopback halo copy");
     }
   }
@@ -580,6 +600,11 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     return cuda_fail(e, "cell kernel occupancy");
   }
   st = plan_traces(m);
+  if (st == HD_OK) {
+    cudaError_t e2 = cudaMalloc(&m->dbg, 16 * sizeof(int));
+    if (e2 == cudaSuccess) e2 = cudaMemset(m->dbg, 0, 16 * sizeof(int));
+    if (e2 != cudaSuccess) st = cuda_fail(e2, "debug words");
+  }
   m->nchunk = 1;
   m->chunk_u[0] = 0;
   m->chunk_u[1] = m->nunits;
@@ -875,6 +900,42 @@ hd_status launch_stage_group(hd_mesh **ms, int P, std::vector<hd::CellParams> &p
   return HD_OK;
 }
 
+// HD_DEBUG builds: the non-finite check of an RK stage's output and, at the end of an API call, the
+// error word (host synchronises; HD_ERR_STATE with the reason). Release builds: no-ops.
+hd_status debug_stage_check(hd_mesh *m, const double *out, cudaStream_t s) {
+#ifdef HD_DEBUG
+  cudaError_t e = hd::launch_finite_check(out, m->owned_dofs, m->dbg, s);
+  if (e != cudaSuccess) return cuda_fail(e, "finite check");
+#else
+  (void)m;
+  (void)out;
+  (void)s;
+#endif
+  return HD_OK;
+}
+hd_status debug_finish(hd_mesh *const *ms, int P, cudaStream_t s) {
+#ifdef HD_DEBUG
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "debug synchronise");
+  for (int r = 0; r < P; ++r) {
+    int w = 0;
+    e = cudaMemcpy(&w, ms[r]->dbg, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "debug word");
+    if (w) {
+      cudaMemset(ms[r]->dbg, 0, sizeof(int));
+      return fail(HD_ERR_STATE, "debug check failed on rank %d:%s%s%s", ms[r]->desc.rank,
+                  (w & 1) ? " index out of range" : "", (w & 2) ? " stale halo trace (S:481)" : "",
+                  (w & 4) ? " non-finite value after an RK stage (S:508)" : "");
+    }
+  }
+#else
+  (void)ms;
+  (void)P;
+  (void)s;
+#endif
+  return HD_OK;
+}
+
 // Vectors are device pointers the kernels read and write with 16-byte vector accesses.
 hd_status check_vec(const void *v, const char *what) {
   if (!v) return fail(HD_ERR_ARG, "null %s", what);
@@ -920,7 +981,9 @@ hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, v
   hd::CellParams p;
   fill_cell_params(m, p);
   set_dtfac(m, p, 1.0);
-  return launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream);
+  st = launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream);
+  if (st != HD_OK) return st;
+  return debug_finish(&m, 1, (cudaStream_t)stream);
 }
 
 hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {
@@ -938,12 +1001,13 @@ hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, 
     for (int s = 0; s < 5; ++s) {
       st = launch_stage(m, p, buf[iu], buf[idu], buf[iw], s == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[s], kRkB[s],
                         (cudaStream_t)stream);
+      if (st == HD_OK) st = debug_stage_check(m, buf[iw], (cudaStream_t)stream);
       if (st != HD_OK) return st;
       std::swap(iu, iw);
     }
   }
   *sol = iu;
-  return HD_OK;
+  return debug_finish(&m, 1, (cudaStream_t)stream);
 }
 
 hd_status hd_rk_stage(hd_mesh *m, const double *U, double *dU, double *out, int stage, double dt, void *stream) {
@@ -958,8 +1022,11 @@ hd_status hd_rk_stage(hd_mesh *m, const double *U, double *dU, double *out, int 
   hd::CellParams p;
   fill_cell_params(m, p);
   set_dtfac(m, p, dt);
-  return launch_stage(m, p, U, dU, out, stage == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[stage], kRkB[stage],
-                      (cudaStream_t)stream);
+  st = launch_stage(m, p, U, dU, out, stage == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[stage], kRkB[stage],
+                    (cudaStream_t)stream);
+  if (st == HD_OK) st = debug_stage_check(m, out, (cudaStream_t)stream);
+  if (st != HD_OK) return st;
+  return debug_finish(&m, 1, (cudaStream_t)stream);
 }
 
 hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double **v, double t, void *stream) {
@@ -977,7 +1044,9 @@ hd_status hd_apply_advection_group(hd_mesh **ms, int P, const double **u, double
     fill_cell_params(ms[r], ps[r]);
     set_dtfac(ms[r], ps[r], 1.0);
   }
-  return launch_stage_group(ms, P, ps, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, s);
+  hd_status st = launch_stage_group(ms, P, ps, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, s);
+  if (st != HD_OK) return st;
+  return debug_finish(ms, P, s);
 }
 
 hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double t, double dt, int nsteps,
@@ -1008,12 +1077,13 @@ hd_status hd_rk_step_group(hd_mesh **ms, int P, double **bufs, int *sol, double 
       }
       hd_status st = launch_stage_group(ms, P, ps, U.data(), DU.data(), W.data(),
                                         st5 == 0 ? hd::kModeRKFirst : hd::kModeRK, kRkA[st5], kRkB[st5], s);
+      for (int r = 0; r < P && st == HD_OK; ++r) st = debug_stage_check(ms[r], W[r], s);
       if (st != HD_OK) return st;
       std::swap(iu, iw);
     }
   }
   *sol = iu;
-  return HD_OK;
+  return debug_finish(ms, P, s);
 }
 
 hd_status hd_fill_initial(hd_mesh *m, double *u, int recipe, unsigned long long seed, void *stream) {

@@ -100,6 +100,19 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
   return sR + swz<D, N>(T);
 }
 
+// HD_DEBUG builds: device-side checks that record into the mesh's error word (the host
+// reports HD_ERR_STATE); release builds compile them out.
+#ifdef HD_DEBUG
+#define HD_DCHECK(p, cond, bit)                  \
+  do {                                           \
+    if (!(cond)) atomicOr((p).err, (bit));       \
+  } while (0)
+#else
+#define HD_DCHECK(p, cond, bit) \
+  do {                          \
+  } while (0)
+#endif
+
 // Resolved schedule of one cell of a group (smem, double buffered; written by the lanes that own the
 // group's (cell, dim) items, read by every thread of the cell).
 struct CellInfo {
@@ -642,6 +655,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   const int fbase = swz<D, N>((2 * tid) % G::ND);
   const int fcell0 = (2 * tid) / G::ND;
   auto copy_cells = [&](int first_cell, double *dst) {
+    HD_DCHECK(p, first_cell >= 0 && first_cell + (CT - 1) * p.cstride < p.ncells, 1);
     if constexpr (FASTFILL) {
       if (nthr == 256 && (CT * G::ND) % 512 == 0) {
         if constexpr (G::ND >= 512) {
@@ -714,6 +728,11 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
         ts = p.hbuf[i] + (size_t)rr.slot * p.FN;
       }
       if (src == kSrcDirect) ts = p.u + (size_t)rr.nb * p.ND;
+      HD_DCHECK(p, rawc[kc].cell >= 0 && rawc[kc].cell < p.ncells && rr.nb >= 0 && rr.nb < p.ncells, 1);
+      HD_DCHECK(p, src != kSrcPub || (rr.slot >= 0 && rr.slot < p.ncells && rr.pflag >= 0 && rr.pflag < p.nunits), 1);
+      HD_DCHECK(p, src != kSrcGroup || (rr.slot >= 0 && rr.slot < CT), 1);
+      HD_DCHECK(p, src != kSrcHalo || (rr.slot >= 0 && rr.slot < p.nhalo[i]), 1);
+      HD_DCHECK(p, src != kSrcHalo || p.rtag[i * 2 + rr.sg] == p.epoch, 2);  // halo of this stage
       ci.base[i] = rr.base;
       ci.tsrc[i] = ts;
       ci.nb[i] = (unsigned char)rr.slot;

@@ -113,6 +113,15 @@ struct CellParams {
   double slin[kMaxD][kMaxD];  // a_lin[i][j] h_j fac_i: change of the line speed of dim i per unit node of dim j
   int coff[kMaxD];        // global cell coordinates of the local box origin (pack kernel)
   int L[kMaxD];           // local box (pack kernel)
+  // HD_DEBUG builds only: error word (bit 1 index out of range, bit 2 stale halo trace,
+  // bit 4 non-finite value), bounds, and the halo freshness tags: stag[dim][dir] = epoch of the
+  // traces this rank packed, rtag[dim][dir] = epoch of the traces it received (dir 0: from / to the left
+  // neighbour's a_i > 0 side, 1: a_i < 0)
+  int *err;
+  int *stag;
+  const int *rtag;
+  long long ncells;
+  long long nhalo[kMaxD];
   // constant-speed dims: s_i K[s] and s_i tau[s] with s_i = a_i dtfac / h_i (compact [dim][sign][N][N]
   // and [dim][sign][N] for the mesh's N); variable dims use the unit-speed c_tab tables on scaled lines
   double Ks[kMaxD * 2 * kMaxN * kMaxN];
@@ -155,6 +164,8 @@ cudaError_t launch_mass_kernel(int d, int n, const StreamParams &p, cudaStream_t
 cudaError_t launch_fill_kernel(int d, int n, const FillParams &p, cudaStream_t s, long long *launches);
 cudaError_t launch_pack_kernel(int d, int n, const PackParams &pp, const CellParams &cp, cudaStream_t s,
                                long long *launches);
+// HD_DEBUG: set bit 4 of *err if any of the n values is not finite
+cudaError_t launch_finite_check(const double *v, long long n, int *err, cudaStream_t s);
 bool cell_kernel_supported(int d, int n);
 
 // Static schedule of a mesh (hd_sched.cpp): [nunits * GPU][CT][d] records (see SchedDim).
@@ -215,6 +226,7 @@ struct hd_mesh {
     long long sr[3][2], sl[3][2], rl[3][2], rr[3][2];
   } chunk[hd::kMaxChunk];
   cudaStream_t comm;                              // NCCL transport: pack + exchange stream
+  int *dbg;                                       // HD_DEBUG: [0] error word, [1..6] stag, [7..12] rtag
   cudaEvent_t ev_u, ev_chunk[hd::kMaxChunk];
   int *pack_cells, *pack_dimsg;
   double *sendbuf;

@@ -207,7 +207,18 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ PackP
 #pragma unroll
     for (int j = 1; j < N; ++j) t = fma(tau[j], us[j], t);
     pp.out[gi] = t;
+#ifdef HD_DEBUG
+    if (f == 0) p.stag[X * 2 + S] = p.epoch;  // freshness tag of this stage's traces
+#endif
   }
+}
+
+// HD_DEBUG: non-finite values after an RK stage
+__global__ void __launch_bounds__(256) finite_kernel(const double *v, long long n, int *err) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(v[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 4);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -407,6 +418,10 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &pp, const CellPar
   HD_DISPATCH(launch_pack_dn, cudaErrorNotSupported, pp, cp, s)
 }
 bool cell_kernel_supported(int d, int n) { HD_DISPATCH(supported_dn, false) }
+cudaError_t launch_finite_check(const double *v, long long n, int *err, cudaStream_t s) {
+  finite_kernel<<<148 * 8, 256, 0, s>>>(v, n, err);
+  return cudaGetLastError();
+}
 CellGeometry cell_geometry(int d, int n, int L0, int L1, long long ncells, int pencil_ok) {
   HD_DISPATCH(geometry_dn, CellGeometry{}, L0, L1, ncells, pencil_ok)
 }

@@ -61,9 +61,7 @@ def run_group():
     us = [torch.from_numpy(np.random.default_rng(r).uniform(-1, 1, m.owned_dofs)).cuda() for r, m in enumerate(ms)]
     vs = [torch.empty_like(x) for x in us]
     apply_advection_group(ms, us, vs)
-    bufs = []
-    for x in us:
-        bufs += [x.clone(), torch.empty_like(x), torch.empty_like(x)]
+    bufs = [[x.clone(), torch.empty_like(x), torch.empty_like(x)] for x in us]
     rk_step_group(ms, bufs, 0, 0.0, 1e-3, 1)
     torch.cuda.synchronize()
     print("5d-group-P2 ok")
