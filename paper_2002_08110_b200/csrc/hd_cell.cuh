@@ -113,6 +113,41 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
   } while (0)
 #endif
 
+// HD_PROFILE builds (experiments only): lane 0 of every warp of CTAs 0 and 74 accumulates,
+// per barrier site of the group loop, the cycles it waited at the barrier (clock64 at arrival; after the
+// barrier a dependent smem read forces the deferred block) and the cycles between barriers; printed per
+// warp at the end of the launch.
+#ifdef HD_PROFILE
+#define HD_PROF_DECL                                                                  \
+  unsigned long long pf_t = clock64(), pf_wait[4] = {0, 0, 0, 0}, pf_work[4] = {0, 0, 0, 0}, pf_groups = 0;
+#define HD_PROF_BAR(site)                                                              \
+  do {                                                                                 \
+    const unsigned long long ta_ = clock64();                                          \
+    pf_work[site] += ta_ - pf_t;                                                       \
+    __syncthreads();                                                                   \
+    const unsigned long long tb_ = clock64() + *(volatile int *)smem_raw * 0;          \
+    pf_wait[site] += tb_ - ta_;                                                        \
+    pf_t = tb_;                                                                        \
+  } while (0)
+#define HD_PROF_GROUP() ++pf_groups
+#define HD_PROF_DUMP()                                                                                         \
+  if ((blockIdx.x == 0 || blockIdx.x == 74) && (threadIdx.x & 31) == 0 && pf_groups)                           \
+    printf("HDPROF cta %d warp %d | wait top %llu b0 %llu b1 %llu bL %llu | work ->top %llu ->b0 %llu ->b1 %llu " \
+           "->bL %llu\n",                                                                                       \
+           blockIdx.x, threadIdx.x >> 5, pf_wait[0] / pf_groups, pf_wait[1] / pf_groups, pf_wait[2] / pf_groups, \
+           pf_wait[3] / pf_groups, pf_work[0] / pf_groups, pf_work[1] / pf_groups, pf_work[2] / pf_groups,       \
+           pf_work[3] / pf_groups)
+#else
+#define HD_PROF_DECL
+#define HD_PROF_BAR(site) __syncthreads()
+#define HD_PROF_GROUP() \
+  do {                  \
+  } while (0)
+#define HD_PROF_DUMP() \
+  do {                 \
+  } while (0)
+#endif
+
 // Resolved schedule of one cell of a group (smem, double buffered; written by the lanes that own the
 // group's (cell, dim) items, read by every thread of the cell).
 struct CellInfo {
@@ -584,7 +619,8 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 }
 
 // Shared-memory carve-up (offsets in doubles, every region 16-byte aligned):
-// bufs[2][CT*NDP] | carry[2][CT*FN] | ptab[NPH][1024] | stg[NPH][2][256][N] | info[2][CT] | raw[CT*D] | rawc[CT]
+// bufs[2][CT*NDP] | carry[2][CT*FN] | ptab[NPH][1024] | stg[NPH][2][256][N] | info[2][CT] | raw[4][CT*D] |
+// rawc[4][CT] (the schedule-record ring)
 __host__ __device__ constexpr int round2(int x) { return (x + 1) & ~1; }
 template <int D, int N>
 struct SmemMap {
@@ -596,8 +632,8 @@ struct SmemMap {
     stg = ptab + G::NPH * 1024;
     info = stg + round2(G::NPH * 2 * 256 * N);
     raw = info + round2(2 * CT * (int)sizeof(CellInfo) / 8);
-    rawc = raw + CT * D * (int)sizeof(SchedDim) / 8;
-    bytes = (rawc + round2(CT * (int)sizeof(SchedCell) / 8)) * 8;
+    rawc = raw + 4 * CT * D * (int)sizeof(SchedDim) / 8;
+    bytes = (rawc + round2(4 * CT * (int)sizeof(SchedCell) / 8)) * 8;
   }
 };
 static_assert(sizeof(CellInfo) % 8 == 0 && sizeof(SchedDim) % 16 == 0 && sizeof(SchedCell) == 8, "smem records");
@@ -686,34 +722,51 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       }
     }
   };
-  // schedule records of group gs -> raw (each item's record is staged and later read by the same thread)
-  auto stage = [&](long long gs) {
-    for (int idx = tid; idx < nitems; idx += nthr) {
-      const SchedDim *src = p.sched + gs * nitems + idx;
-      cp_async16(raw + idx, src);
-      cp_async16(reinterpret_cast<char *>(raw + idx) + 16, reinterpret_cast<const char *>(src) + 16);
-      if (idx % D == 0) cp_async8(rawc + idx / D, p.schedc + gs * CT + idx / D);
-    }
-    cp_async_commit();
+  // Schedule records: a ring of kRing groups in smem, fetched (cp.async, spread over the threads) three
+  // groups ahead of their use, so no thread waits for them. The (cell, dim) items of a group -- flag
+  // acquire and resolution into CellInfo -- are spread over the warps (lane j of warp w: item j*nwarps + w),
+  // so no warp carries the group's bookkeeping alone.
+  constexpr int kRing = 4;
+  auto fetch = [&](int slot, long long gs) {
+    const char *src = reinterpret_cast<const char *>(p.sched + gs * nitems);
+    char *dst = reinterpret_cast<char *>(raw + slot * MAXCT * D);
+    for (int q = tid; q < nitems * 2; q += nthr) cp_async16(dst + 16 * q, src + 16 * q);
+    for (int q = tid; q < CT; q += nthr) cp_async8(rawc + slot * MAXCT + q, p.schedc + gs * CT + q);
   };
+  // the CTA's group sequence: iteration it -> (unit, step); j groups ahead of (u0, g0)
+  auto ahead = [&](int u0, int g0, int j, int &uo, int &go) {
+    uo = u0;
+    go = g0 + j;
+    while (go >= p.GPU) {
+      go -= p.GPU;
+      uo += gridDim.x;
+    }
+    return uo < p.u_end;
+  };
+  const int nwarps = nthr >> 5;
+  const int item0 = nitems <= nthr ? (tid & 31) * nwarps + (tid >> 5) : tid;
   int fv0 = 0, fv1 = 0;  // producer flag values of this thread's items (at most 2 items per thread)
-  auto acquire = [&]() {
+  auto acquire = [&](int slot) {
+    const SchedDim *rs = raw + slot * MAXCT * D;
     int j = 0;
-    for (int idx = tid; idx < nitems; idx += nthr, ++j) {
-      const SchedDim &rr = raw[idx];
+    for (int idx = item0; idx < nitems; idx += nthr, ++j) {
+      const SchedDim &rr = rs[idx];
       if (rr.src == kSrcPub) {
         const int v = ld_acquire(p.flags + rr.pflag);
         if (j == 0) fv0 = v;
         else fv1 = v;
+      } else if (rr.src == kSrcDirect && p.prefetch) {
+        prefetch_l2(p.u + (size_t)rr.nb * p.ND, (unsigned)(p.ND * 8));
       }
-      else if (rr.src == kSrcDirect && p.prefetch) prefetch_l2(p.u + (size_t)rr.nb * p.ND, (unsigned)(p.ND * 8));
     }
   };
-  auto resolve = [&](CellInfo *inf) {
+  auto resolve = [&](int slot, CellInfo *inf) {
+    const SchedDim *rs = raw + slot * MAXCT * D;
+    const SchedCell *rc = rawc + slot * MAXCT;
     int j = 0;
-    for (int idx = tid; idx < nitems; idx += nthr, ++j) {
+    for (int idx = item0; idx < nitems; idx += nthr, ++j) {
       const int kc = idx / D, i = idx - kc * D;
-      const SchedDim &rr = raw[idx];
+      const SchedDim &rr = rs[idx];
       CellInfo &ci = inf[kc];
       unsigned char src = rr.src;
       const double *ts = nullptr;
@@ -728,7 +781,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
         ts = p.hbuf[i] + (size_t)rr.slot * p.FN;
       }
       if (src == kSrcDirect) ts = p.u + (size_t)rr.nb * p.ND;
-      HD_DCHECK(p, rawc[kc].cell >= 0 && rawc[kc].cell < p.ncells && rr.nb >= 0 && rr.nb < p.ncells, 1);
+      HD_DCHECK(p, rc[kc].cell >= 0 && rc[kc].cell < p.ncells && rr.nb >= 0 && rr.nb < p.ncells, 1);
       HD_DCHECK(p, src != kSrcPub || (rr.slot >= 0 && rr.slot < p.ncells && rr.pflag >= 0 && rr.pflag < p.nunits), 1);
       HD_DCHECK(p, src != kSrcGroup || (rr.slot >= 0 && rr.slot < CT), 1);
       HD_DCHECK(p, src != kSrcHalo || (rr.slot >= 0 && rr.slot < p.nhalo[i]), 1);
@@ -740,33 +793,36 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       ci.out[i] = rr.out;
       ci.sg[i] = rr.sg;
       if (i == 0) {
-        ci.cell = rawc[kc].cell;
-        ci.oslot = rawc[kc].oslot;
+        ci.cell = rc[kc].cell;
+        ci.oslot = rc[kc].oslot;
       }
     }
   };
 
   int u = p.u_begin + (int)blockIdx.x, gi = 0, it = 0;
-  // prologue: group 0's schedule and cells
-  stage((long long)u * p.GPU);
+  // prologue: the records of the first three groups, group 0's schedule and cells
+  for (int j = 0; j < kRing - 1; ++j) {
+    int ua, ga;
+    if (ahead(u, gi, j, ua, ga)) fetch(j, (long long)ua * p.GPU + ga);
+  }
+  cp_async_commit();
   cp_async_wait<0>();
-  acquire();
-  resolve(info0);
   __syncthreads();
+  acquire(0);
+  resolve(0, info0);
   copy_cells(rawc[0].cell, bufs);
   cp_async_commit();
   cp_async_wait<0>();
   int prev_unit = -1, prev_step = 0;
+  HD_PROF_DECL
   while (u < p.u_end) {
     const int s = it & 1;
-    int un = u, gn = gi + 1;
-    if (gn >= p.GPU) {
-      un = u + gridDim.x;
-      gn = 0;
-    }
-    const bool has_next = un < p.u_end;
+    const int slot1 = (it + 1) % kRing;  // records of the next group
+    int un, gn;
+    const bool has_next = ahead(u, gi, 1, un, gn);
     // group g-1 done (its traces written, its epilogue finished); this group's cells and info are in smem
-    __syncthreads();
+    HD_PROF_BAR(0);
+    HD_PROF_GROUP();
     if (prev_unit >= 0 && tid == nthr - 1) st_release(p.flags + prev_unit, p.epoch | (prev_step + 1));
     const CellInfo &ci = info0[s * MAXCT + kk0];
     GroupBufs gb;
@@ -775,10 +831,8 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     gb.A = bufs + (s ^ 1) * CND + (size_t)kk0 * G::NDP;
     gb.carry = carry0 + (size_t)(s * MAXCT + kk0) * G::FN;
     gb.carry_out = carry0 + (size_t)((s ^ 1) * MAXCT + kk0) * G::FN;
-    // cp.async groups of this thread, in commit order: the next group's records, this group's staged
-    // traces per phase, then (last phase) RK dU and the next group's cells
-    if (has_next) stage((long long)un * p.GPU + gn);
-    else cp_async_commit();
+    // cp.async groups of this thread, in commit order: this group's staged traces per phase, the records of
+    // the group three ahead, then (last phase) RK dU and the next group's cells
     if (active) {
       stage_phase<D, N, 0>(ci, r, stg, tid);
       if constexpr (NPH > 1) stage_phase<D, N, (NPH > 1 ? 1 : 0)>(ci, r, stg, tid);
@@ -786,16 +840,20 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     } else {
       for (int q = 0; q < NPH; ++q) cp_async_commit();
     }
+    {
+      int ua, ga;
+      if (ahead(u, gi, kRing - 1, ua, ga)) fetch((it + kRing - 1) % kRing, (long long)ua * p.GPU + ga);
+      cp_async_commit();
+    }
     if (MODE == kModeRK && tid == 0 && p.prefetch)
       for (int kc = 0; kc < CT; ++kc)
         prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
     auto flags_next = [&]() {
       if (has_next) {
-        cp_async_wait<NPH>();  // the records (the oldest group)
-        acquire();
+        acquire(slot1);
         if (tid == 0 && p.prefetch)
           for (int kc = 0; kc < CT; ++kc)
-            prefetch_l2(p.u + ((size_t)rawc[0].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
+            prefetch_l2(p.u + ((size_t)rawc[slot1 * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
       }
     };
     auto refill = [&](int sR, int R) {
@@ -814,28 +872,30 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
         }
         cp_async_commit();
       }
-      if (has_next) copy_cells(rawc[0].cell, bufs + (s ^ 1) * CND);
+      if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs + (s ^ 1) * CND);
       cp_async_commit();
     };
     auto none = [](int, int) {};
-    constexpr int WLAST = MODE == kModeRK ? 2 : 1;  // commits after the last phase's traces: dU, cells
+    // pending commits after phase PH's traces when its lifts wait: the later phases' traces and the records;
+    // in the last phase the records, (RK) dU and the next group's cells
+    constexpr int WLAST = 1 + (MODE == kModeRK ? 2 : 1);
     if constexpr (NPH == 1) {
       flags_next();
       run_phase<D, N, MODE, 0, WLAST>(p, ci, ptab, stg, r, gb, active, refill);
     } else {
-      run_phase<D, N, MODE, 0, NPH - 1>(p, ci, ptab, stg, r, gb, active, none);
-      __syncthreads();
+      run_phase<D, N, MODE, 0, NPH>(p, ci, ptab, stg, r, gb, active, none);
+      HD_PROF_BAR(1);
       flags_next();
       if constexpr (NPH == 2) {
         run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
       } else {
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), (NPH > 2 ? 1 : 0)>(p, ci, ptab, stg, r, gb, active, none);
-        __syncthreads();
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 2>(p, ci, ptab, stg, r, gb, active, none);
+        HD_PROF_BAR(2);
         run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
       }
     }
-    if (has_next) resolve(info0 + (s ^ 1) * MAXCT);
-    cp_async_wait<0>();  // the next group's cells
+    if (has_next) resolve(slot1, info0 + (s ^ 1) * MAXCT);
+    cp_async_wait<0>();  // the next group's cells (and the records fetched this group)
     prev_unit = p.flags ? u : -1;
     prev_step = gi;
     u = un;
@@ -846,6 +906,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     __syncthreads();
     if (tid == nthr - 1) st_release(p.flags + prev_unit, p.epoch | (prev_step + 1));
   }
+  HD_PROF_DUMP();
 }
 
 }  // namespace hd
