@@ -119,7 +119,9 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
 // warp at the end of the launch.
 #ifdef HD_PROFILE
 #define HD_PROF_DECL                                                                  \
-  unsigned long long pf_t = clock64(), pf_wait[4] = {0, 0, 0, 0}, pf_work[4] = {0, 0, 0, 0}, pf_groups = 0;
+  unsigned long long pf_t = clock64(), pf_wait[4] = {0, 0, 0, 0}, pf_work[4] = {0, 0, 0, 0}, pf_groups = 0; \
+  unsigned long long pf_sub[3][6] = {};
+#define HD_PF(ph) pf_sub[ph]
 #define HD_PROF_BAR(site)                                                              \
   do {                                                                                 \
     const unsigned long long ta_ = clock64();                                          \
@@ -130,18 +132,36 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
     pf_t = tb_;                                                                        \
   } while (0)
 #define HD_PROF_GROUP() ++pf_groups
+#define HD_SUB_DECL unsigned long long sb_t = clock64();
+#define HD_SUB(k)                                   \
+  do {                                              \
+    const unsigned long long t_ = clock64();        \
+    if (pf_sub) pf_sub[(k)] += t_ - sb_t;           \
+    sb_t = t_;                                      \
+  } while (0)
 #define HD_PROF_DUMP()                                                                                         \
   if ((blockIdx.x == 0 || blockIdx.x == 74) && (threadIdx.x & 31) == 0 && pf_groups)                           \
     printf("HDPROF cta %d warp %d | wait top %llu b0 %llu b1 %llu bL %llu | work ->top %llu ->b0 %llu ->b1 %llu " \
            "->bL %llu\n",                                                                                       \
            blockIdx.x, threadIdx.x >> 5, pf_wait[0] / pf_groups, pf_wait[1] / pf_groups, pf_wait[2] / pf_groups, \
            pf_wait[3] / pf_groups, pf_work[0] / pf_groups, pf_work[1] / pf_groups, pf_work[2] / pf_groups,       \
-           pf_work[3] / pf_groups)
+           pf_work[3] / pf_groups);                                                                              \
+  if ((blockIdx.x == 0) && (threadIdx.x & 31) == 0 && pf_groups)                                              \
+    for (int ph_ = 0; ph_ < 3; ++ph_)                                                                          \
+      printf("HDSUB warp %d phase %d | loads %llu passP %llu passQ %llu trP+liftP %llu trQ+liftQ %llu store %llu\n", \
+             threadIdx.x >> 5, ph_, pf_sub[ph_][0] / pf_groups, pf_sub[ph_][1] / pf_groups,                     \
+             pf_sub[ph_][2] / pf_groups, pf_sub[ph_][3] / pf_groups, pf_sub[ph_][4] / pf_groups,                \
+             pf_sub[ph_][5] / pf_groups)
 #else
 #define HD_PROF_DECL
+#define HD_PF(ph) nullptr
 #define HD_PROF_BAR(site) __syncthreads()
 #define HD_PROF_GROUP() \
   do {                  \
+  } while (0)
+#define HD_SUB_DECL
+#define HD_SUB(k) \
+  do {            \
   } while (0)
 #define HD_PROF_DUMP() \
   do {                 \
@@ -498,7 +518,9 @@ __device__ __forceinline__ void lift_Q(double (&acc)[N][N], const double (&t)[N]
 //    accumulator buffer (and RK dU into the thread's own U slots), overlapping the last phase.
 template <int D, int N, int MODE, int PH, int WAIT, class Refill>
 __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *ptab, double *stg, int r,
-                                          const GroupBufs &gb, bool active, Refill &&refill) {
+                                          const GroupBufs &gb, bool active, Refill &&refill,
+                                          unsigned long long *pf_sub = nullptr) {
+  HD_SUB_DECL
   using G = CGeo<D, N>;
   constexpr int P = G::P(PH), Q = G::Q(PH);
   constexpr bool QA = G::QA(PH);
@@ -553,6 +575,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   }
   if (!active) return;
   const size_t g0 = (size_t)ci.cell * G::ND + R;
+  HD_SUB(0);
 
   // volume terms of P and Q and this cell's downwind traces along P and Q (stored right away)
   {
@@ -562,23 +585,27 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     if (oP == kOutCarry) store_vec<N>(gb.carry_out + N * r, tr, false);
     else if (oP == kOutPub) store_vec<N>(p.tbuf[P] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
   }
+  HD_SUB(1);
   if constexpr (QA) {
     double tr[N];
     pass_Q_any<N, Q>(p, acc, uv, lsQ, tr, ci.sg[Q], p.var[Q]);
     if (ci.out[Q] == kOutPub) store_vec<N>(p.tbuf[Q] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
   }
+  HD_SUB(2);
   // upwind traces (the staged ones have arrived once this thread's copies of this phase are complete)
   cp_async_wait<WAIT>();
   if (!LAST || ci.src[P] != kSrcGroup)
     trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
   if (ci.sg[P]) lift_P<N, 1>(acc, tP);
   else lift_P<N, 0>(acc, tP);
+  HD_SUB(3);
   if constexpr (QA) {
     if (!LAST || ci.src[Q] != kSrcGroup)
       trace_in<D, N, Q, SQ, SP>(p, ci, r, sR, R, gb, lsQ, stg_slot<N>(stg, PH, 1, tid), tQ);
     if (ci.sg[Q]) lift_Q<N, 1>(acc, tQ);
     else lift_Q<N, 0>(acc, tQ);
   }
+  HD_SUB(4);
 
   if constexpr (!LAST && P == 0 && N % 2 == 0) {
 #pragma unroll
@@ -883,15 +910,15 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       flags_next();
       run_phase<D, N, MODE, 0, WLAST>(p, ci, ptab, stg, r, gb, active, refill);
     } else {
-      run_phase<D, N, MODE, 0, NPH>(p, ci, ptab, stg, r, gb, active, none);
+      run_phase<D, N, MODE, 0, NPH>(p, ci, ptab, stg, r, gb, active, none, HD_PF(0));
       HD_PROF_BAR(1);
       flags_next();
       if constexpr (NPH == 2) {
         run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
       } else {
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 2>(p, ci, ptab, stg, r, gb, active, none);
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 2>(p, ci, ptab, stg, r, gb, active, none, HD_PF(1));
         HD_PROF_BAR(2);
-        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
+        run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill, HD_PF(2));
       }
     }
     if (has_next) resolve(slot1, info0 + (s ^ 1) * MAXCT);
