@@ -514,7 +514,9 @@ __device__ __forceinline__ void lift_Q(double (&acc)[N][N], const double (&t)[N]
 
 // One phase: tile over (P, Q) at this thread's rest coordinates. Its published traces were staged into
 // smem at the group start (cp.async group WAIT = the number of this thread's commits after it).
-//  * LAST: after every thread has loaded its tile (barrier), `refill` streams the next group into the
+//  * LAST: `stage_du` (RK) copies the stage's dU into this thread's own (just read) accumulator slots; the
+//    next group's cells already stream into the third buffer since the group start, so no barrier here.
+//  (was: LAST: after every thread has loaded its tile (barrier), `refill` streams the next group into the
 //    accumulator buffer (and RK dU into the thread's own U slots), overlapping the last phase.
 template <int D, int N, int MODE, int PH, int WAIT, class Refill>
 __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &ci, const double *ptab, double *stg, int r,
@@ -561,18 +563,8 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
         for (int b = 0; b < N; ++b) acc[a][b] = gb.A[sidx<D, N>(sR, a * SP + b * SQ)];
     }
-    if constexpr (LAST) {
-      // in-group neighbours must be read before the barrier (their U slots are reused after it)
-      if (ci.src[P] == kSrcGroup) trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, nullptr, tP);
-      if constexpr (QA) {
-        if (ci.src[Q] == kSrcGroup) trace_in<D, N, Q, SQ, SP>(p, ci, r, sR, R, gb, lsQ, nullptr, tQ);
-      }
-    }
   }
-  if constexpr (LAST) {
-    __syncthreads();  // every tile of U and ACC is in registers: both buffers may be rewritten
-    refill(sR, R);
-  }
+  if constexpr (LAST) refill(sR, R);  // RK: dU into this thread's own accumulator slots (read above)
   if (!active) return;
   const size_t g0 = (size_t)ci.cell * G::ND + R;
   HD_SUB(0);
@@ -594,14 +586,12 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   HD_SUB(2);
   // upwind traces (the staged ones have arrived once this thread's copies of this phase are complete)
   cp_async_wait<WAIT>();
-  if (!LAST || ci.src[P] != kSrcGroup)
-    trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
+  trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
   if (ci.sg[P]) lift_P<N, 1>(acc, tP);
   else lift_P<N, 0>(acc, tP);
   HD_SUB(3);
   if constexpr (QA) {
-    if (!LAST || ci.src[Q] != kSrcGroup)
-      trace_in<D, N, Q, SQ, SP>(p, ci, r, sR, R, gb, lsQ, stg_slot<N>(stg, PH, 1, tid), tQ);
+    trace_in<D, N, Q, SQ, SP>(p, ci, r, sR, R, gb, lsQ, stg_slot<N>(stg, PH, 1, tid), tQ);
     if (ci.sg[Q]) lift_Q<N, 1>(acc, tQ);
     else lift_Q<N, 0>(acc, tQ);
   }
@@ -627,13 +617,13 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       for (int b = 0; b < N; ++b) __stcs(p.out + g0 + a * SP + b * SQ, acc[a][b] * (wr * (T.w[a] * T.w[b])));
   } else {
     // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU. U is still in uv; dU arrived
-    // (cp.async issued by refill) in this thread's own slots of the U buffer.
+    // (cp.async issued by stage_du) in this thread's own slots of the accumulator buffer.
     if constexpr (MODE == kModeRK) {
-      cp_async_wait<1>();
+      cp_async_wait<0>();
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
-        for (int b = 0; b < N; ++b) acc[a][b] = fma(p.rk_a, gb.U[sidx<D, N>(sR, a * SP + b * SQ)], acc[a][b]);
+        for (int b = 0; b < N; ++b) acc[a][b] = fma(p.rk_a, gb.A[sidx<D, N>(sR, a * SP + b * SQ)], acc[a][b]);
     }
 #pragma unroll
     for (int a = 0; a < N; ++a)
@@ -646,15 +636,15 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 }
 
 // Shared-memory carve-up (offsets in doubles, every region 16-byte aligned):
-// bufs[2][CT*NDP] | carry[2][CT*FN] | ptab[NPH][1024] | stg[NPH][2][256][N] | info[2][CT] | raw[4][CT*D] |
-// rawc[4][CT] (the schedule-record ring)
+// bufs[3][CT*NDP] (two cell buffers alternating, one accumulator) | carry[2][CT*FN] | ptab[NPH][1024] |
+// stg[NPH][2][256][N] | info[2][CT] | raw[4][CT*D] | rawc[4][CT] (the schedule-record ring)
 __host__ __device__ constexpr int round2(int x) { return (x + 1) & ~1; }
 template <int D, int N>
 struct SmemMap {
   int carry, ptab, stg, info, raw, rawc, bytes;
   __host__ __device__ constexpr SmemMap(int CT) : carry(0), ptab(0), stg(0), info(0), raw(0), rawc(0), bytes(0) {
     using G = CGeo<D, N>;
-    carry = round2(2 * CT * G::NDP);
+    carry = round2(3 * CT * G::NDP);
     ptab = carry + round2(2 * CT * G::FN);
     stg = ptab + G::NPH * 1024;
     info = stg + round2(G::NPH * 2 * 256 * N);
@@ -855,7 +845,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     GroupBufs gb;
     gb.Ugrp = bufs + s * CND;
     gb.U = gb.Ugrp + (size_t)kk0 * G::NDP;
-    gb.A = bufs + (s ^ 1) * CND + (size_t)kk0 * G::NDP;
+    gb.A = bufs + 2 * CND + (size_t)kk0 * G::NDP;
     gb.carry = carry0 + (size_t)(s * MAXCT + kk0) * G::FN;
     gb.carry_out = carry0 + (size_t)((s ^ 1) * MAXCT + kk0) * G::FN;
     // cp.async groups of this thread, in commit order: this group's staged traces per phase, the records of
@@ -878,45 +868,48 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     auto flags_next = [&]() {
       if (has_next) {
         acquire(slot1);
-        if (tid == 0 && p.prefetch)
+        // the cells of the group after next into L2 (its fill is issued at the next group's start)
+        int ua, ga;
+        if (tid == 0 && p.prefetch && ahead(u, gi, 2, ua, ga)) {
+          const int slot2 = (it + 2) % kRing;
           for (int kc = 0; kc < CT; ++kc)
-            prefetch_l2(p.u + ((size_t)rawc[slot1 * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
+            prefetch_l2(p.u + ((size_t)rawc[slot2 * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
+        }
       }
     };
+    // the next group's cells stream into the other cell buffer (free since the previous group ended)
+    if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs + (s ^ 1) * CND);
+    cp_async_commit();
     auto refill = [&](int sR, int R) {
-      // RK: dU of this thread's tile into its own (already read) U slots; then the next group's cells into
-      // the accumulator buffer (read completely before the barrier)
+      // RK: dU of this thread's tile into its own (already read) accumulator slots
       if constexpr (MODE == kModeRK) {
         if (active) {
           constexpr int P = G::P(NPH - 1), Q = G::Q(NPH - 1);
           constexpr int SP = ipow(N, P), SQ = ipow(N, Q);
           const double *src = p.du + (size_t)ci.cell * G::ND + R;
-          double *dst = const_cast<double *>(gb.U);
 #pragma unroll
           for (int a = 0; a < N; ++a)
 #pragma unroll
-            for (int b = 0; b < N; ++b) cp_async8(dst + sidx<D, N>(sR, a * SP + b * SQ), src + a * SP + b * SQ);
+            for (int b = 0; b < N; ++b) cp_async8(gb.A + sidx<D, N>(sR, a * SP + b * SQ), src + a * SP + b * SQ);
         }
         cp_async_commit();
       }
-      if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs + (s ^ 1) * CND);
-      cp_async_commit();
     };
     auto none = [](int, int) {};
-    // pending commits after phase PH's traces when its lifts wait: the later phases' traces and the records;
-    // in the last phase the records, (RK) dU and the next group's cells
-    constexpr int WLAST = 1 + (MODE == kModeRK ? 2 : 1);
+    // pending commits after phase PH's traces when its lifts wait: the later phases' traces, the records
+    // and the next group's cells; in the last phase the records, the cells and (RK) dU
+    constexpr int WLAST = 2 + (MODE == kModeRK ? 1 : 0);
     if constexpr (NPH == 1) {
       flags_next();
       run_phase<D, N, MODE, 0, WLAST>(p, ci, ptab, stg, r, gb, active, refill);
     } else {
-      run_phase<D, N, MODE, 0, NPH>(p, ci, ptab, stg, r, gb, active, none, HD_PF(0));
+      run_phase<D, N, MODE, 0, NPH + 1>(p, ci, ptab, stg, r, gb, active, none, HD_PF(0));
       HD_PROF_BAR(1);
       flags_next();
       if constexpr (NPH == 2) {
         run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
       } else {
-        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 2>(p, ci, ptab, stg, r, gb, active, none, HD_PF(1));
+        run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 3>(p, ci, ptab, stg, r, gb, active, none, HD_PF(1));
         HD_PROF_BAR(2);
         run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill, HD_PF(2));
       }
