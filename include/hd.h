@@ -151,6 +151,14 @@ hd_status hd_nccl_unique_id(void *out128);
 hd_status hd_partition_info(const hd_mesh_desc *desc, int *xparts, long long *off, long long *len);
 hd_status hd_halo_list(const hd_mesh_desc *desc, int dim, int which, long long *ids, long long *count, int *peer);
 
+/* Host-only query of the v-chunk pipeline of desc->rank: *nchunk chunks; chunk_units[0..nchunk]
+ * (may be NULL): chunk c = units [chunk_units[c], chunk_units[c+1]); plan (may be NULL; kMaxChunk = 8 x 3 x 8
+ * long longs): for chunk c and x dim i, plan[(c*3+i)*8 + ...] = {first entry and count of the traces sent
+ * to the right rank, as a range of hd_halo_list(which = 1); first entry and count of those sent to the left
+ * rank (which = 0); first receive slot and count from the left rank; first receive slot and count from the
+ * right rank}. */
+hd_status hd_halo_chunks(const hd_mesh_desc *desc, int *nchunk, long long *chunk_units, long long *plan);
+
 /* Number of kernels this library launched since the mesh was created (bench evidence). */
 long long hd_launch_count(const hd_mesh *m);
 

@@ -36,7 +36,7 @@ _lib = None
 EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection",
            "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_stage", "hd_rk_step_host", "hd_apply_advection_group",
            "hd_rk_step_group", "hd_fill_initial", "hd_tables_1d", "hd_lsrk_coefficients", "hd_mesh_traces",
-           "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_launch_count", "hd_last_error"]
+           "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_halo_chunks", "hd_launch_count", "hd_last_error"]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -69,6 +69,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_nccl_unique_id.argtypes = [vp]
     lib.hd_partition_info.argtypes = [P(HdMeshDesc), P(ctypes.c_int), P(ll), P(ll)]
     lib.hd_halo_list.argtypes = [P(HdMeshDesc), ctypes.c_int, ctypes.c_int, P(ll), P(ll), P(ctypes.c_int)]
+    lib.hd_halo_chunks.argtypes = [P(HdMeshDesc), P(ctypes.c_int), P(ll), P(ll)]
     lib.hd_launch_count.argtypes = [vp]
     lib.hd_launch_count.restype = ll
     lib.hd_last_error.restype = ctypes.c_char_p
@@ -135,6 +136,26 @@ def halo_list(spec: dict, rank: int, nranks: int, dim: int, which: int, xparts=N
     ids = (ctypes.c_longlong * max(1, cnt.value))()
     _check(lib.hd_halo_list(ctypes.byref(ds), dim, which, ids, ctypes.byref(cnt), ctypes.byref(peer)))
     return peer.value, list(ids)[:cnt.value]
+
+
+def halo_chunks(spec: dict, rank: int, nranks: int, xparts=None):
+    """Host-only v-chunk plan (include/hd.h hd_halo_chunks): (chunk unit bounds, per chunk a dict per x dim:
+    sr, sl ((first entry of hd_halo_list which 1 / 0, count): traces to the right / left rank), rl, rr ((first
+    slot, count) from the left / right rank))."""
+    ds = make_desc(spec, rank, nranks, None, xparts)
+    lib = load_library()
+    nc = ctypes.c_int(0)
+    units = (ctypes.c_longlong * 9)()
+    plan = (ctypes.c_longlong * (8 * 3 * 8))()
+    _check(lib.hd_halo_chunks(ctypes.byref(ds), ctypes.byref(nc), units, plan))
+    out = []
+    for c in range(nc.value):
+        dims = []
+        for i in range(3):
+            q = plan[(c * 3 + i) * 8:(c * 3 + i + 1) * 8]
+            dims.append(dict(sr=(q[0], q[1]), sl=(q[2], q[3]), rl=(q[4], q[5]), rr=(q[6], q[7])))
+        out.append(dims)
+    return list(units)[:nc.value + 1], out
 
 
 def tables_1d(n: int):

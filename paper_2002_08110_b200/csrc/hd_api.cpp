@@ -285,49 +285,41 @@ hd_status upload_schedule(hd_mesh *m) {
 // the units are ordered with the slowest dim (a v dim, never split) outermost, so a range of its
 // traversal coordinate is a contiguous unit range, and -- the halo plane order also having that dim
 // slowest -- a contiguous range of every send list and receive buffer.
-hd_status setup_halo(hd_mesh *m) {
-  const int d = m->d;
-  const long long fn = m->nd / m->n;
-  const long long Ls = m->pt.len[d - 1];
-  // chunks: ranges of the slowest dim's traversal coordinate t (reversed cell order when that dim follows
-  // a negative speed, as in the schedule)
-  m->nchunk = m->geo.pencil ? (int)std::min<long long>(4, Ls) : 1;
+// The v-chunk plan of a multi-rank mesh, host only (also behind the hd_halo_chunks query): chunk unit ranges
+// and, per chunk and x dim, the (offset, count) of the send-list entries to the right / left rank and of the
+// receive slots from the left / right rank; the chunk-major send list itself (cells, dim | sign << 8).
+struct ChunkPlan {
+  int nchunk = 1;
+  int chunk_u[hd::kMaxChunk + 1] = {};
+  hd_mesh::ChunkHalo chunk[hd::kMaxChunk] = {};
+  std::vector<int> cells, dimsg;
+};
+void build_chunk_plan(const hd_mesh_desc &ds, const hd::Partition &pt, const double *h, const hd::CellGeometry &geo,
+                      long long nunits, bool follow_last, const hd::HaloDim *halo, ChunkPlan &cp) {
+  const int d = pt.d;
+  const long long Ls = pt.len[d - 1];
+  cp = ChunkPlan();
+  cp.nchunk = geo.pencil ? (int)std::min<long long>(4, Ls) : 1;
   bool reversed = false;
-  if (m->geo.pencil && m->follow[d - 1]) {
+  if (geo.pencil && follow_last) {
     long long cg[6];
-    for (int j = 0; j < d; ++j) cg[j] = m->pt.off[j];
-    reversed = hd::host_cell_sign(m->desc, m->h, d, d - 1, cg) != 0;
+    for (int j = 0; j < d; ++j) cg[j] = pt.off[j];
+    reversed = hd::host_cell_sign(ds, h, d, d - 1, cg) != 0;
   }
   long long tcut[hd::kMaxChunk + 1];
-  for (int c = 0; c <= m->nchunk; ++c) tcut[c] = c * Ls / m->nchunk;
-  const long long units_per_slice = m->geo.pencil ? m->nunits / Ls : 0;
-  for (int c = 0; c <= m->nchunk; ++c) m->chunk_u[c] = m->geo.pencil ? (int)(tcut[c] * units_per_slice) : (c ? m->nunits : 0);
-  // cell range [c0, c1) of the slowest coordinate of chunk c
-  auto crange = [&](int c, long long &c0, long long &c1) {
-    if (!m->geo.pencil) {
-      c0 = 0;
-      c1 = Ls;
-    } else if (reversed) {
-      c0 = Ls - tcut[c + 1];
-      c1 = Ls - tcut[c];
-    } else {
-      c0 = tcut[c];
-      c1 = tcut[c + 1];
+  for (int c = 0; c <= cp.nchunk; ++c) tcut[c] = c * Ls / cp.nchunk;
+  const long long units_per_slice = geo.pencil ? nunits / Ls : 0;
+  for (int c = 0; c <= cp.nchunk; ++c) cp.chunk_u[c] = geo.pencil ? (int)(tcut[c] * units_per_slice) : (c ? (int)nunits : 0);
+  for (int c = 0; c < cp.nchunk; ++c) {
+    hd_mesh::ChunkHalo &ch = cp.chunk[c];
+    ch.pe0 = (long long)cp.cells.size();
+    long long c0 = 0, c1 = Ls;  // cell range of the slowest coordinate
+    if (geo.pencil) {
+      c0 = reversed ? Ls - tcut[c + 1] : tcut[c];
+      c1 = reversed ? Ls - tcut[c] : tcut[c + 1];
     }
-  };
-  std::vector<int> cells, dimsg;
-  for (int i = 0; i < m->desc.d_x; ++i) {
-    hd::HaloDim &hd = m->halo[i];
-    hd::make_halo(m->desc, m->pt, m->h, i, hd);
-  }
-  for (int c = 0; c < m->nchunk; ++c) {
-    hd_mesh::ChunkHalo &ch = m->chunk[c];
-    std::memset(&ch, 0, sizeof(ch));
-    ch.pe0 = (long long)cells.size();
-    long long c0, c1;
-    crange(c, c0, c1);
-    for (int i = 0; i < m->desc.d_x; ++i) {
-      const hd::HaloDim &hd = m->halo[i];
+    for (int i = 0; i < ds.d_x; ++i) {
+      const hd::HaloDim &hd = halo[i];
       if (!hd.active) continue;
       // plane positions of the chunk: [j0, j1) (the slowest dim is slowest in the plane order too)
       const long long plane = (long long)hd.slot.size(), per = plane / Ls;
@@ -339,25 +331,41 @@ hd_status setup_halo(hd_mesh *m) {
         else (s1 ? in1 : in0) += 1;
       }
       // to the right rank: my high-face cells with a_i > 0 (sign 0), in plane order; to the left: sign 1
-      ch.sr[i][0] = (long long)cells.size();
+      ch.sr[i][0] = (long long)cp.cells.size();
       ch.sr[i][1] = in0;
       for (long long q = before0; q < before0 + in0; ++q) {
-        cells.push_back(hd.send_right[q]);
-        dimsg.push_back(i);
+        cp.cells.push_back(hd.send_right[q]);
+        cp.dimsg.push_back(i);
       }
-      ch.sl[i][0] = (long long)cells.size();
+      ch.sl[i][0] = (long long)cp.cells.size();
       ch.sl[i][1] = in1;
       for (long long q = before1; q < before1 + in1; ++q) {
-        cells.push_back(hd.send_left[q]);
-        dimsg.push_back(i | (1 << 8));
+        cp.cells.push_back(hd.send_left[q]);
+        cp.dimsg.push_back(i | (1 << 8));
       }
       ch.rl[i][0] = before0;
       ch.rl[i][1] = in0;
       ch.rr[i][0] = hd.n_from_left + before1;
       ch.rr[i][1] = in1;
+      ch.srq[i] = before0;
+      ch.slq[i] = before1;
     }
-    ch.pe1 = (long long)cells.size();
+    ch.pe1 = (long long)cp.cells.size();
   }
+}
+
+// Halo plan and buffers of a multi-rank mesh (hd_plan.cpp), cut into v-chunks: in pencil mode
+// the units are ordered with the slowest dim (a v dim, never split) outermost, so a range of its
+// traversal coordinate is a contiguous unit range, and -- the halo plane order also having that dim
+// slowest -- a contiguous range of every send list and receive buffer.
+hd_status setup_halo(hd_mesh *m) {
+  const long long fn = m->nd / m->n;
+  for (int i = 0; i < m->desc.d_x; ++i) hd::make_halo(m->desc, m->pt, m->h, i, m->halo[i]);
+  ChunkPlan cp;
+  build_chunk_plan(m->desc, m->pt, m->h, m->geo, m->nunits, m->follow[m->d - 1] != 0, m->halo, cp);
+  m->nchunk = cp.nchunk;
+  std::memcpy(m->chunk_u, cp.chunk_u, sizeof(m->chunk_u));
+  std::memcpy(m->chunk, cp.chunk, sizeof(m->chunk));
   for (int i = 0; i < m->desc.d_x; ++i) {
     const hd::HaloDim &hd = m->halo[i];
     if (!hd.active) continue;
@@ -367,9 +375,9 @@ hd_status setup_halo(hd_mesh *m) {
                 "halo receive buffer");
     if (st != HD_OK) return st;
   }
-  m->nsend = (long long)cells.size();
-  hd_status st = upload(&m->pack_cells, cells.data(), cells.size(), "halo pack list");
-  if (st == HD_OK) st = upload(&m->pack_dimsg, dimsg.data(), dimsg.size(), "halo pack list");
+  m->nsend = (long long)cp.cells.size();
+  hd_status st = upload(&m->pack_cells, cp.cells.data(), cp.cells.size(), "halo pack list");
+  if (st == HD_OK) st = upload(&m->pack_dimsg, cp.dimsg.data(), cp.dimsg.size(), "halo pack list");
   if (st == HD_OK) st = upload(&m->sendbuf, (const double *)nullptr, (size_t)m->nsend * fn, "halo send buffer");
   return st;
 }
@@ -760,6 +768,47 @@ hd_status hd_partition_info(const hd_mesh_desc *desc, int *xparts, long long *of
     if (off) off[i] = pt.off[i];
     if (len) len[i] = pt.len[i];
   }
+  return HD_OK;
+}
+
+hd_status hd_halo_chunks(const hd_mesh_desc *desc, int *nchunk, long long *chunk_units, long long *plan) {
+  if (!desc || !nchunk) return fail(HD_ERR_ARG, "null argument");
+  const int d = desc->d_x + desc->d_v;
+  if (desc->d_x < 1 || desc->d_x > 3 || desc->d_v < 1 || desc->d_v > 3 || desc->k < 1 || desc->k > 5)
+    return fail(HD_ERR_ARG, "invalid d_x, d_v or k");
+  hd::Partition pt;
+  std::string err;
+  if (!hd::make_partition(*desc, pt, err)) return fail(HD_ERR_ARG, "%s", err.c_str());
+  double h[6];
+  for (int i = 0; i < d; ++i) h[i] = (desc->hi[i] - desc->lo[i]) / (double)desc->cells[i];
+  const int n = desc->k + 1;
+  const int pencil_ok = desc->a_lin[6 * 0 + 1] == 0.0;
+  const hd::CellGeometry geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], pt.ncells_local, pencil_ok);
+  if (geo.CT < 1) return fail(HD_ERR_UNSUPPORTED, "(d=%d, n=%d) is not in the built kernel set", d, n);
+  const long long nunits = geo.pencil ? pt.ncells_local / (pt.len[0] * geo.CT) : pt.ncells_local / geo.CT;
+  bool follow_last = geo.pencil && pt.len[d - 1] >= 2;
+  for (int j = 0; j < d - 1; ++j) follow_last = follow_last && desc->a_lin[6 * (d - 1) + j] == 0.0;
+  hd::HaloDim halo[3];
+  for (int i = 0; i < desc->d_x; ++i) hd::make_halo(*desc, pt, h, i, halo[i]);
+  ChunkPlan cp;
+  build_chunk_plan(*desc, pt, h, geo, nunits, follow_last, halo, cp);
+  *nchunk = cp.nchunk;
+  for (int c = 0; c <= cp.nchunk; ++c)
+    if (chunk_units) chunk_units[c] = cp.chunk_u[c];
+  if (plan)
+    for (int c = 0; c < cp.nchunk; ++c)
+      for (int i = 0; i < 3; ++i) {
+        long long *q = plan + ((size_t)c * 3 + i) * 8;
+        const hd_mesh::ChunkHalo &ch = cp.chunk[c];
+        q[0] = ch.srq[i];
+        q[1] = ch.sr[i][1];
+        q[2] = ch.slq[i];
+        q[3] = ch.sl[i][1];
+        q[4] = ch.rl[i][0];
+        q[5] = ch.rl[i][1];
+        q[6] = ch.rr[i][0];
+        q[7] = ch.rr[i][1];
+      }
   return HD_OK;
 }
 

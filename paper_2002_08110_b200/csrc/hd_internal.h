@@ -224,6 +224,7 @@ struct hd_mesh {
   struct ChunkHalo {
     long long pe0, pe1;
     long long sr[3][2], sl[3][2], rl[3][2], rr[3][2];
+    long long srq[3], slq[3];  // first entry of the chunk's part of the dim's send_right / send_left list
   } chunk[hd::kMaxChunk];
   cudaStream_t comm;                              // NCCL transport: pack + exchange stream
   int *dbg;                                       // HD_DEBUG: [0] error word, [1..6] stag, [7..12] rtag
