@@ -64,12 +64,15 @@ typedef struct {
   double a_lin[36];     /* ... row-major [i][j]; a_lin[i][i] must be 0 (divergence free); the
                            sign of a_i must be constant on every cell (reading C11) */
   int flux;             /* 0 = upwind (the only flux built on the GPU path) */
-  int rank, nranks;     /* x-space partition over nranks ranks: the ranks form a grid
-                           xparts[0] x .. x xparts[d_x-1] over the x-cells; every v-cell is rank-local */
+  int rank, nranks;     /* phase-space partition over nranks ranks: the ranks form a grid
+                           parts[0] x .. x parts[d-1] over the cells (parts = xparts, then vparts); rank r
+                           has block coordinates b_i = (r / prod_{j<i} parts_j) % parts_i */
   const void *nccl_id;  /* 128-byte ncclUniqueId when nranks > 1 and the NCCL transport is wanted; NULL
                            selects the in-process loopback transport (hd_*_group calls) */
-  int xparts[3];        /* ranks per x dim (p_i must divide cells[i], prod = nranks); all 0 = automatic:
-                           the factorisation with the smallest halo, x-slabs (slowest dim) on ties */
+  int xparts[3];        /* ranks per x dim (p_i must divide cells[i]); all of xparts and vparts 0 =
+                           automatic: the x factorisation with the smallest halo, x-slabs on ties */
+  int vparts[3];        /* ranks per v dim (checkerboard x-v partition; 0 or 1 = not split).
+                           Explicit partitions need prod(xparts) * prod(vparts) = nranks */
 } hd_mesh_desc;
 
 /* Validate desc, build the 1D tables and the partition. HD_ERR_ARG for invalid input (S:48:
@@ -82,9 +85,9 @@ hd_status hd_destroy_mesh(hd_mesh *m);
  * flattened x-cell index c_x. Any output pointer may be NULL. */
 hd_status hd_mesh_info(const hd_mesh *m, long long *owned_dofs, long long *cx_begin, long long *cx_end);
 
-/* The rank's local box of the global cell grid: off[i], len[i] per dim (d entries used; v dims are never
- * split) and the rank grid xparts[3]. Local vectors hold the box's cells lexicographically (first axis
- * fastest). Any output pointer may be NULL. */
+/* The rank's local box of the global cell grid: off[i], len[i] per dim (d entries used) and the x part of the
+ * rank grid xparts[3] (the v part is cells[i] / len[i]). Local vectors hold the box's cells
+ * lexicographically (first axis fastest). Any output pointer may be NULL. */
 hd_status hd_mesh_box(const hd_mesh *m, long long *off, long long *len, int *xparts);
 
 /* v <- A(u) (weak form). u, v: device vectors of owned_dofs doubles that must not overlap
@@ -152,8 +155,8 @@ hd_status hd_partition_info(const hd_mesh_desc *desc, int *xparts, long long *of
 hd_status hd_halo_list(const hd_mesh_desc *desc, int dim, int which, long long *ids, long long *count, int *peer);
 
 /* Host-only query of the v-chunk pipeline of desc->rank: *nchunk chunks; chunk_units[0..nchunk]
- * (may be NULL): chunk c = units [chunk_units[c], chunk_units[c+1]); plan (may be NULL; kMaxChunk = 8 x 3 x 8
- * long longs): for chunk c and x dim i, plan[(c*3+i)*8 + ...] = {first entry and count of the traces sent
+ * (may be NULL): chunk c = units [chunk_units[c], chunk_units[c+1]); plan (may be NULL; kMaxChunk = 8 x 6 x 8
+ * long longs): for chunk c and split dim i, plan[(c*6+i)*8 + ...] = {first entry and count of the traces sent
  * to the right rank, as a range of hd_halo_list(which = 1); first entry and count of those sent to the left
  * rank (which = 0); first receive slot and count from the left rank; first receive slot and count from the
  * right rank}. */

@@ -26,7 +26,7 @@ class HdMeshDesc(ctypes.Structure):
         ("cells", ctypes.c_longlong * 6), ("lo", ctypes.c_double * 6), ("hi", ctypes.c_double * 6),
         ("a_const", ctypes.c_double * 6), ("a_lin", ctypes.c_double * 36),
         ("flux", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
-        ("nccl_id", ctypes.c_void_p), ("xparts", ctypes.c_int * 3),
+        ("nccl_id", ctypes.c_void_p), ("xparts", ctypes.c_int * 3), ("vparts", ctypes.c_int * 3),
     ]
 
 
@@ -85,7 +85,7 @@ def _check(st):
 
 
 def make_desc(spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
-              xparts=None) -> HdMeshDesc:
+              xparts=None, vparts=None) -> HdMeshDesc:
     ds = HdMeshDesc()
     d = spec["d_x"] + spec["d_v"]
     ds.d_x, ds.d_v, ds.k = spec["d_x"], spec["d_v"], spec["k"]
@@ -103,6 +103,9 @@ def make_desc(spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None 
     if xparts is not None:
         for i, p in enumerate(xparts):
             ds.xparts[i] = int(p)
+    if vparts is not None:
+        for i, p in enumerate(vparts):
+            ds.vparts[i] = int(p)
     ds._nccl_buf = None
     if nccl_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -118,18 +121,18 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def partition_info(spec: dict, rank: int, nranks: int, xparts=None):
+def partition_info(spec: dict, rank: int, nranks: int, xparts=None, vparts=None):
     """Host-only: (xparts[3], box offset[d], box length[d]) of a rank (no GPU needed)."""
     d = spec["d_x"] + spec["d_v"]
-    ds = make_desc(spec, rank, nranks, None, xparts)
+    ds = make_desc(spec, rank, nranks, None, xparts, vparts)
     xp, off, ln = (ctypes.c_int * 3)(), (ctypes.c_longlong * 6)(), (ctypes.c_longlong * 6)()
     _check(load_library().hd_partition_info(ctypes.byref(ds), xp, off, ln))
     return list(xp), list(off)[:d], list(ln)[:d]
 
 
-def halo_list(spec: dict, rank: int, nranks: int, dim: int, which: int, xparts=None):
+def halo_list(spec: dict, rank: int, nranks: int, dim: int, which: int, xparts=None, vparts=None):
     """Host-only halo plan query (include/hd.h hd_halo_list): (peer, [global cell ids])."""
-    ds = make_desc(spec, rank, nranks, None, xparts)
+    ds = make_desc(spec, rank, nranks, None, xparts, vparts)
     lib = load_library()
     cnt, peer = ctypes.c_longlong(0), ctypes.c_int(0)
     _check(lib.hd_halo_list(ctypes.byref(ds), dim, which, None, ctypes.byref(cnt), ctypes.byref(peer)))
@@ -138,21 +141,21 @@ def halo_list(spec: dict, rank: int, nranks: int, dim: int, which: int, xparts=N
     return peer.value, list(ids)[:cnt.value]
 
 
-def halo_chunks(spec: dict, rank: int, nranks: int, xparts=None):
+def halo_chunks(spec: dict, rank: int, nranks: int, xparts=None, vparts=None):
     """Host-only v-chunk plan (include/hd.h hd_halo_chunks): (chunk unit bounds, per chunk a dict per x dim:
     sr, sl ((first entry of hd_halo_list which 1 / 0, count): traces to the right / left rank), rl, rr ((first
     slot, count) from the left / right rank))."""
-    ds = make_desc(spec, rank, nranks, None, xparts)
+    ds = make_desc(spec, rank, nranks, None, xparts, vparts)
     lib = load_library()
     nc = ctypes.c_int(0)
     units = (ctypes.c_longlong * 9)()
-    plan = (ctypes.c_longlong * (8 * 3 * 8))()
+    plan = (ctypes.c_longlong * (8 * 6 * 8))()
     _check(lib.hd_halo_chunks(ctypes.byref(ds), ctypes.byref(nc), units, plan))
     out = []
     for c in range(nc.value):
         dims = []
-        for i in range(3):
-            q = plan[(c * 3 + i) * 8:(c * 3 + i + 1) * 8]
+        for i in range(6):
+            q = plan[(c * 6 + i) * 8:(c * 6 + i + 1) * 8]
             dims.append(dict(sr=(q[0], q[1]), sl=(q[2], q[3]), rl=(q[4], q[5]), rr=(q[6], q[7])))
         out.append(dims)
     return list(units)[:nc.value + 1], out
@@ -186,11 +189,12 @@ def _stream_handle(stream):
 class Mesh:
     """A mesh of the C ABI. Vectors are torch float64 CUDA tensors of ``owned_dofs`` elements."""
 
-    def __init__(self, spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None, xparts=None):
+    def __init__(self, spec: dict, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None, xparts=None,
+                 vparts=None):
         lib = load_library()
         self.spec = spec
         self.rank, self.nranks = rank, nranks
-        self._desc = make_desc(spec, rank, nranks, nccl_id, xparts)
+        self._desc = make_desc(spec, rank, nranks, nccl_id, xparts, vparts)
         h = ctypes.c_void_p()
         _check(lib.hd_create_mesh(ctypes.byref(self._desc), ctypes.byref(h)))
         self._h = h

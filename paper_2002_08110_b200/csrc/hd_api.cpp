@@ -128,13 +128,13 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.dtfac = 1.0;
   p.err = m->dbg;
   p.stag = m->dbg + 1;
-  p.rtag = m->dbg + 7;
+  p.rtag = m->dbg + 13;
   p.ncells = m->ncells_local;
-  for (int i = 0; i < 3; ++i) p.nhalo[i] = m->halo[i].n_from_left + m->halo[i].n_from_right;
+  for (int i = 0; i < 6; ++i) p.nhalo[i] = m->halo[i].n_from_left + m->halo[i].n_from_right;
   for (int i = 0; i < d; ++i) {
     p.L[i] = (int)m->pt.len[i];
     p.coff[i] = (int)m->pt.off[i];
-    if (i < 3 && m->pt.xparts[i] > 1) p.hbuf[i] = m->hbuf[i];
+    if (m->pt.parts[i] > 1) p.hbuf[i] = m->hbuf[i];
     p.lo[i] = m->desc.lo[i];
     p.h[i] = m->h[i];
     p.inv_h[i] = 1.0 / m->h[i];
@@ -194,7 +194,7 @@ void free_mesh(hd_mesh *m) {
   if (m->sched) cudaFree(m->sched);
   if (m->dbg) cudaFree(m->dbg);
   if (m->schedc) cudaFree(m->schedc);
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 6; ++i) {
     if (m->hbuf[i]) cudaFree(m->hbuf[i]);
     if (m->hslot[i]) cudaFree(m->hslot[i]);
   }
@@ -299,7 +299,8 @@ void build_chunk_plan(const hd_mesh_desc &ds, const hd::Partition &pt, const dou
   const int d = pt.d;
   const long long Ls = pt.len[d - 1];
   cp = ChunkPlan();
-  cp.nchunk = geo.pencil ? (int)std::min<long long>(4, Ls) : 1;
+  // chunks are ranges of the slowest dim, which must then not be split itself (its halo would cross chunks)
+  cp.nchunk = geo.pencil && pt.parts[d - 1] == 1 ? (int)std::min<long long>(4, Ls) : 1;
   bool reversed = false;
   if (geo.pencil && follow_last) {
     long long cg[6];
@@ -308,17 +309,18 @@ void build_chunk_plan(const hd_mesh_desc &ds, const hd::Partition &pt, const dou
   }
   long long tcut[hd::kMaxChunk + 1];
   for (int c = 0; c <= cp.nchunk; ++c) tcut[c] = c * Ls / cp.nchunk;
-  const long long units_per_slice = geo.pencil ? nunits / Ls : 0;
-  for (int c = 0; c <= cp.nchunk; ++c) cp.chunk_u[c] = geo.pencil ? (int)(tcut[c] * units_per_slice) : (c ? (int)nunits : 0);
+  const long long units_per_slice = cp.nchunk > 1 ? nunits / Ls : 0;
+  for (int c = 0; c <= cp.nchunk; ++c)
+    cp.chunk_u[c] = cp.nchunk > 1 ? (int)(tcut[c] * units_per_slice) : (c ? (int)nunits : 0);
   for (int c = 0; c < cp.nchunk; ++c) {
     hd_mesh::ChunkHalo &ch = cp.chunk[c];
     ch.pe0 = (long long)cp.cells.size();
     long long c0 = 0, c1 = Ls;  // cell range of the slowest coordinate
-    if (geo.pencil) {
+    if (cp.nchunk > 1) {
       c0 = reversed ? Ls - tcut[c + 1] : tcut[c];
       c1 = reversed ? Ls - tcut[c] : tcut[c + 1];
     }
-    for (int i = 0; i < ds.d_x; ++i) {
+    for (int i = 0; i < d; ++i) {
       const hd::HaloDim &hd = halo[i];
       if (!hd.active) continue;
       // plane positions of the chunk: [j0, j1) (the slowest dim is slowest in the plane order too)
@@ -360,13 +362,13 @@ void build_chunk_plan(const hd_mesh_desc &ds, const hd::Partition &pt, const dou
 // slowest -- a contiguous range of every send list and receive buffer.
 hd_status setup_halo(hd_mesh *m) {
   const long long fn = m->nd / m->n;
-  for (int i = 0; i < m->desc.d_x; ++i) hd::make_halo(m->desc, m->pt, m->h, i, m->halo[i]);
+  for (int i = 0; i < m->d; ++i) hd::make_halo(m->desc, m->pt, m->h, i, m->halo[i]);
   ChunkPlan cp;
   build_chunk_plan(m->desc, m->pt, m->h, m->geo, m->nunits, m->follow[m->d - 1] != 0, m->halo, cp);
   m->nchunk = cp.nchunk;
   std::memcpy(m->chunk_u, cp.chunk_u, sizeof(m->chunk_u));
   std::memcpy(m->chunk, cp.chunk, sizeof(m->chunk));
-  for (int i = 0; i < m->desc.d_x; ++i) {
+  for (int i = 0; i < m->d; ++i) {
     const hd::HaloDim &hd = m->halo[i];
     if (!hd.active) continue;
     hd_status st = upload(&m->hslot[i], hd.slot.data(), hd.slot.size(), "halo slot table");
@@ -408,7 +410,7 @@ hd_status halo_exchange_nccl(hd_mesh *m, int c, cudaStream_t s) {
   const hd_mesh::ChunkHalo &ch = m->chunk[c];
   nccl_result r = g_nccl.group_start();
   if (r) return nccl_fail(r, "ncclGroupStart");
-  for (int i = 0; i < m->desc.d_x; ++i) {
+  for (int i = 0; i < m->d; ++i) {
     const hd::HaloDim &hd = m->halo[i];
     if (!hd.active) continue;
     if (ch.sr[i][1]) r = g_nccl.send(m->sendbuf + ch.sr[i][0] * fn, ch.sr[i][1] * fn, kNcclFloat64, hd.right, m->nccl_comm, s);
@@ -422,8 +424,8 @@ hd_status halo_exchange_nccl(hd_mesh *m, int c, cudaStream_t s) {
     // freshness tags travel with the traces; every rank runs the same build
     if (!r) r = g_nccl.send(m->dbg + 1 + i * 2, 1, kNcclInt32, hd.right, m->nccl_comm, s);
     if (!r) r = g_nccl.send(m->dbg + 2 + i * 2, 1, kNcclInt32, hd.left, m->nccl_comm, s);
-    if (!r) r = g_nccl.recv(m->dbg + 7 + i * 2, 1, kNcclInt32, hd.left, m->nccl_comm, s);
-    if (!r) r = g_nccl.recv(m->dbg + 8 + i * 2, 1, kNcclInt32, hd.right, m->nccl_comm, s);
+    if (!r) r = g_nccl.recv(m->dbg + 13 + i * 2, 1, kNcclInt32, hd.left, m->nccl_comm, s);
+    if (!r) r = g_nccl.recv(m->dbg + 14 + i * 2, 1, kNcclInt32, hd.right, m->nccl_comm, s);
 #endif
     if (r) {
       g_nccl.group_end();
@@ -442,7 +444,7 @@ hd_status halo_exchange_loopback(hd_mesh **ms, int P, int c, cudaStream_t s) {
     hd_mesh *m = ms[r];
     const long long fn = m->nd / m->n;
     const hd_mesh::ChunkHalo &ch = m->chunk[c];
-    for (int i = 0; i < m->desc.d_x; ++i) {
+    for (int i = 0; i < m->d; ++i) {
       const hd::HaloDim &hd = m->halo[i];
       if (!hd.active) continue;
       const hd_mesh *L = ms[hd.left], *R = ms[hd.right];
@@ -455,9 +457,9 @@ hd_status halo_exchange_loopback(hd_mesh **ms, int P, int c, cudaStream_t s) {
                             ch.rr[i][1] * fn * sizeof(double), cudaMemcpyDeviceToDevice, s);
 #ifdef HD_DEBUG
       // freshness tags travel with the traces
-      if (e == cudaSuccess) e = cudaMemcpyAsync(m->dbg + 7 + i * 2, L->dbg + 1 + i * 2, sizeof(int), cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(m->dbg + 13 + i * 2, L->dbg + 1 + i * 2, sizeof(int), cudaMemcpyDeviceToDevice, s);
       if (e == cudaSuccess)
-        e = cudaMemcpyAsync(m->dbg + 8 + i * 2, R->dbg + 2 + i * 2, sizeof(int), cudaMemcpyDeviceToDevice, s);
+        e = cudaMemcpyAsync(m->dbg + 14 + i * 2, R->dbg + 2 + i * 2, sizeof(int), cudaMemcpyDeviceToDevice, s);
 #endif
       if (e != cudaSuccess) return cuda_fail(e, "loopback halo copy");
     }
@@ -566,7 +568,9 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     }
     bool contiguous = true;
     for (int i = 0; i + 1 < desc->d_x; ++i)
-      if (pt.xparts[i] > 1) contiguous = false;
+      if (pt.parts[i] > 1) contiguous = false;
+    for (int i = desc->d_x; i < d; ++i)
+      if (pt.parts[i] > 1) contiguous = false;
     m->cx_begin = contiguous ? lo : -1;
     m->cx_end = contiguous ? lo + cnt : -1;
   }
@@ -609,8 +613,8 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   }
   st = plan_traces(m);
   if (st == HD_OK) {
-    cudaError_t e2 = cudaMalloc(&m->dbg, 16 * sizeof(int));
-    if (e2 == cudaSuccess) e2 = cudaMemset(m->dbg, 0, 16 * sizeof(int));
+    cudaError_t e2 = cudaMalloc(&m->dbg, 32 * sizeof(int));
+    if (e2 == cudaSuccess) e2 = cudaMemset(m->dbg, 0, 32 * sizeof(int));
     if (e2 != cudaSuccess) st = cuda_fail(e2, "debug words");
   }
   m->nchunk = 1;
@@ -740,7 +744,7 @@ hd_status hd_mesh_box(const hd_mesh *m, long long *off, long long *len, int *xpa
     if (len) len[i] = i < m->d ? m->pt.len[i] : 1;
   }
   for (int i = 0; i < 3; ++i)
-    if (xparts) xparts[i] = m->pt.xparts[i];
+    if (xparts) xparts[i] = i < m->desc.d_x ? m->pt.parts[i] : 1;
   return HD_OK;
 }
 
@@ -763,7 +767,7 @@ hd_status hd_partition_info(const hd_mesh_desc *desc, int *xparts, long long *of
   std::string err;
   if (!hd::make_partition(*desc, pt, err)) return fail(HD_ERR_ARG, "%s", err.c_str());
   for (int i = 0; i < 3; ++i)
-    if (xparts) xparts[i] = pt.xparts[i];
+    if (xparts) xparts[i] = i < desc->d_x ? pt.parts[i] : 1;
   for (int i = 0; i < 6; ++i) {
     if (off) off[i] = pt.off[i];
     if (len) len[i] = pt.len[i];
@@ -788,8 +792,8 @@ hd_status hd_halo_chunks(const hd_mesh_desc *desc, int *nchunk, long long *chunk
   const long long nunits = geo.pencil ? pt.ncells_local / (pt.len[0] * geo.CT) : pt.ncells_local / geo.CT;
   bool follow_last = geo.pencil && pt.len[d - 1] >= 2;
   for (int j = 0; j < d - 1; ++j) follow_last = follow_last && desc->a_lin[6 * (d - 1) + j] == 0.0;
-  hd::HaloDim halo[3];
-  for (int i = 0; i < desc->d_x; ++i) hd::make_halo(*desc, pt, h, i, halo[i]);
+  hd::HaloDim halo[6];
+  for (int i = 0; i < d; ++i) hd::make_halo(*desc, pt, h, i, halo[i]);
   ChunkPlan cp;
   build_chunk_plan(*desc, pt, h, geo, nunits, follow_last, halo, cp);
   *nchunk = cp.nchunk;
@@ -797,8 +801,8 @@ hd_status hd_halo_chunks(const hd_mesh_desc *desc, int *nchunk, long long *chunk
     if (chunk_units) chunk_units[c] = cp.chunk_u[c];
   if (plan)
     for (int c = 0; c < cp.nchunk; ++c)
-      for (int i = 0; i < 3; ++i) {
-        long long *q = plan + ((size_t)c * 3 + i) * 8;
+      for (int i = 0; i < 6; ++i) {
+        long long *q = plan + ((size_t)c * 6 + i) * 8;
         const hd_mesh::ChunkHalo &ch = cp.chunk[c];
         q[0] = ch.srq[i];
         q[1] = ch.sr[i][1];
@@ -814,7 +818,8 @@ hd_status hd_halo_chunks(const hd_mesh_desc *desc, int *nchunk, long long *chunk
 
 hd_status hd_halo_list(const hd_mesh_desc *desc, int dim, int which, long long *ids, long long *count, int *peer) {
   if (!desc || !count) return fail(HD_ERR_ARG, "null argument");
-  if (dim < 0 || dim >= desc->d_x || which < 0 || which > 3) return fail(HD_ERR_ARG, "dim or which out of range");
+  if (dim < 0 || dim >= desc->d_x + desc->d_v || which < 0 || which > 3)
+    return fail(HD_ERR_ARG, "dim or which out of range");
   hd::Partition pt;
   std::string err;
   if (!hd::make_partition(*desc, pt, err)) return fail(HD_ERR_ARG, "%s", err.c_str());

@@ -36,8 +36,8 @@ enum Mode : int { kModeAdvection = 0, kModeRK = 1, kModeRKFirst = 2 };
 // x-space partition of the ranks (hd_plan.cpp)
 struct Partition {
   int d = 0, d_x = 0, P = 1, rank = 0;
-  int xparts[3] = {1, 1, 1};  // ranks per x dim
-  int bcoord[3] = {0, 0, 0};  // this rank's block coordinates
+  int parts[6] = {1, 1, 1, 1, 1, 1};   // ranks per dim (x dims, then v dims)
+  int bcoord[6] = {0, 0, 0, 0, 0, 0};  // this rank's block coordinates
   long long off[6] = {0, 0, 0, 0, 0, 0}, len[6] = {1, 1, 1, 1, 1, 1};  // local box of the global cell grid
   long long ncells_local = 0;
 };
@@ -211,9 +211,9 @@ struct hd_mesh {
   int grid;
   // halo (nranks > 1): per x dim receive buffer and slot table; one send buffer for all dims, laid
   // out per dim as [to the right rank][to the left rank]
-  hd::HaloDim halo[3];
-  double *hbuf[3];
-  int *hslot[3];
+  hd::HaloDim halo[6];
+  double *hbuf[6];
+  int *hslot[6];
   long long nsend;                                // entries of the send list (chunk-major)
   // v-chunk pipeline of a multi-rank stage: chunk c = the units [chunk_u[c], chunk_u[c+1]),
   // i.e. the cells whose slowest (v) coordinate lies in one range. Per chunk: its send-list entries
@@ -223,11 +223,11 @@ struct hd_mesh {
   int chunk_u[hd::kMaxChunk + 1];
   struct ChunkHalo {
     long long pe0, pe1;
-    long long sr[3][2], sl[3][2], rl[3][2], rr[3][2];
-    long long srq[3], slq[3];  // first entry of the chunk's part of the dim's send_right / send_left list
+    long long sr[6][2], sl[6][2], rl[6][2], rr[6][2];
+    long long srq[6], slq[6];  // first entry of the chunk's part of the dim's send_right / send_left list
   } chunk[hd::kMaxChunk];
   cudaStream_t comm;                              // NCCL transport: pack + exchange stream
-  int *dbg;                                       // HD_DEBUG: [0] error word, [1..6] stag, [7..12] rtag
+  int *dbg;                                       // HD_DEBUG: [0] error word, [1..12] stag, [13..24] rtag
   cudaEvent_t ev_u, ev_chunk[hd::kMaxChunk];
   int *pack_cells, *pack_dimsg;
   double *sendbuf;

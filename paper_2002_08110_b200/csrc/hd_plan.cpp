@@ -1,6 +1,8 @@
 // hd_plan.cpp -- host-only x-space partition and halo plan.
 //
-// Partition: the ranks form a grid xparts[0] x ... x xparts[d_x-1] over the x-cells (x-slabs when only
+// Partition: the ranks form a grid parts[0] x ... x parts[d-1] over the cells; automatically only x dims are
+// split (every v-cell rank-local), an explicit hd_mesh_desc.vparts also splits v dims (the checkerboard x-v
+// partition of P:913-948). Automatic: xparts[0] x ... x xparts[d_x-1] over the x-cells (x-slabs when only
 // the slowest x dim is split, x-blocks otherwise); every v-cell is rank-local ("phase-space
 // partition", with the v part undivided), so v-faces and M^-1 never communicate. Each rank owns the
 // box [off, off + len) of the global Cartesian cell grid, stored lexicographically (first axis fastest,
@@ -41,22 +43,23 @@ bool make_partition(const hd_mesh_desc &ds, Partition &pt, std::string &err) {
   pt.d_x = ds.d_x;
   pt.P = P;
   pt.rank = ds.rank;
-  for (int i = 0; i < 3; ++i) pt.xparts[i] = 1;
+  for (int i = 0; i < 6; ++i) pt.parts[i] = 1;
   bool explicit_parts = false;
-  for (int i = 0; i < 3; ++i) explicit_parts |= ds.xparts[i] > 0;
+  for (int i = 0; i < 3; ++i) explicit_parts |= ds.xparts[i] > 0 || ds.vparts[i] > 0;
   if (explicit_parts) {
     long long prod = 1;
-    for (int i = 0; i < ds.d_x; ++i) {
-      const int pi = ds.xparts[i] > 0 ? ds.xparts[i] : 1;
+    for (int i = 0; i < d; ++i) {
+      const int given = i < ds.d_x ? ds.xparts[i] : ds.vparts[i - ds.d_x];
+      const int pi = given > 0 ? given : 1;
       if (ds.cells[i] % pi != 0) {
-        err = "xparts[" + std::to_string(i) + "] must divide cells[" + std::to_string(i) + "]";
+        err = "the ranks along dim " + std::to_string(i) + " must divide cells[" + std::to_string(i) + "]";
         return false;
       }
-      pt.xparts[i] = pi;
+      pt.parts[i] = pi;
       prod *= pi;
     }
     if (prod != P) {
-      err = "product of xparts must equal nranks";
+      err = "product of xparts and vparts must equal nranks";
       return false;
     }
   } else if (P > 1) {
@@ -95,37 +98,35 @@ bool make_partition(const hd_mesh_desc &ds, Partition &pt, std::string &err) {
       err = "nranks cannot be factored over the x dims (need p_i | cells_i, prod p_i = nranks)";
       return false;
     }
-    for (int i = 0; i < 3; ++i) pt.xparts[i] = bp[i];
+    for (int i = 0; i < 3; ++i) pt.parts[i] = bp[i];
   }
   int r = ds.rank;
-  for (int i = 0; i < 3; ++i) {
-    pt.bcoord[i] = r % pt.xparts[i];
-    r /= pt.xparts[i];
+  for (int i = 0; i < d; ++i) {
+    pt.bcoord[i] = r % pt.parts[i];
+    r /= pt.parts[i];
   }
   pt.ncells_local = 1;
   for (int i = 0; i < d; ++i) {
-    if (i < ds.d_x) {
-      pt.len[i] = ds.cells[i] / pt.xparts[i];
-      pt.off[i] = pt.bcoord[i] * pt.len[i];
-    } else {
-      pt.len[i] = ds.cells[i];
-      pt.off[i] = 0;
-    }
+    pt.len[i] = ds.cells[i] / pt.parts[i];
+    pt.off[i] = pt.bcoord[i] * pt.len[i];
     pt.ncells_local *= pt.len[i];
   }
   return true;
 }
 
 int neighbour_rank(const Partition &pt, int i, int delta) {
-  int bc[3] = {pt.bcoord[0], pt.bcoord[1], pt.bcoord[2]};
-  bc[i] = (bc[i] + delta + pt.xparts[i]) % pt.xparts[i];
-  return bc[0] + pt.xparts[0] * (bc[1] + pt.xparts[1] * bc[2]);
+  int bc[6];
+  for (int j = 0; j < 6; ++j) bc[j] = pt.bcoord[j];
+  bc[i] = (bc[i] + delta + pt.parts[i]) % pt.parts[i];
+  int r = 0;
+  for (int j = pt.d - 1; j >= 0; --j) r = r * pt.parts[j] + bc[j];
+  return r;
 }
 
 void make_halo(const hd_mesh_desc &ds, const Partition &pt, const double *h, int i, HaloDim &hd) {
   const int d = pt.d;
   hd = HaloDim();
-  hd.active = pt.xparts[i] > 1;
+  hd.active = pt.parts[i] > 1;
   if (!hd.active) return;
   hd.left = neighbour_rank(pt, i, -1);
   hd.right = neighbour_rank(pt, i, +1);

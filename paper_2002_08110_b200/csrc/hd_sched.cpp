@@ -156,7 +156,7 @@ void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<Sc
     }
     g.follow[i] = m.follow[i];
     g.pub[i] = m.pub[i];
-    g.xsplit[i] = i < 3 && m.pt.xparts[i] > 1 ? 1 : 0;
+    g.xsplit[i] = m.pt.parts[i] > 1 ? 1 : 0;
   }
   g.UC = g.pencil ? g.L[0] * g.CT : g.CT;
   const int d = g.d, CT = g.CT, GPU = g.GPU;

@@ -1,4 +1,5 @@
-"""GPU: the multi-rank path (x-space partition + upwind-trace halo) against one rank and
+"""GPU: the multi-rank path (x-space and checkerboard x-v partitions + upwind-trace halo with the v-chunk
+pipeline) against one rank and
 against the oracle, with all ranks' meshes on one device and the in-process loopback transport (the
 same buffers NCCL would fill; one GPU is all this pool gives, and ranks must not spin on each other).
 
@@ -35,17 +36,23 @@ def _vlasov(d_x, d_v, k, cells, vmax=2.0, extra=0.0):
     return _spec(d_x, d_v, k, cells, [0.0] * d_x + [-vmax] * d_v, [1.0] * d_x + [vmax] * d_v, ac, lin)
 
 
+# (name, spec, P, xparts, vparts)
 CASES = [
-    ("3d-const-P2", _spec(2, 1, 4, [4, 6, 3], [0] * 3, [1] * 3, [1.0, -0.7, 0.3]), 2, None),
-    ("4d-vlasov-P2", _vlasov(2, 2, 3, [4, 6, 2, 4], extra=0.1), 2, None),
-    ("4d-vlasov-P4", _vlasov(2, 2, 3, [4, 6, 2, 4], extra=0.1), 4, None),
-    ("5d-vlasov-P2", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 2, None),
-    ("5d-vlasov-P8", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 8, None),
-    ("5d-vlasov-P3-x0", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 3, [3, 1, 1]),
-    ("6d-vlasov-P8", _vlasov(3, 3, 3, [4, 4, 4, 2, 2, 2]), 8, None),
+    ("3d-const-P2", _spec(2, 1, 4, [4, 6, 3], [0] * 3, [1] * 3, [1.0, -0.7, 0.3]), 2, None, None),
+    ("4d-vlasov-P2", _vlasov(2, 2, 3, [4, 6, 2, 4], extra=0.1), 2, None, None),
+    ("4d-vlasov-P4", _vlasov(2, 2, 3, [4, 6, 2, 4], extra=0.1), 4, None, None),
+    ("5d-vlasov-P2", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 2, None, None),
+    ("5d-vlasov-P8", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 8, None, None),
+    ("5d-vlasov-P3-x0", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 3, [3, 1, 1], None),
+    ("6d-vlasov-P8", _vlasov(3, 3, 3, [4, 4, 4, 2, 2, 2]), 8, None, None),
     # long pencils with a_0 = v_0 = z_1: chunk mode (parts of a pencil per group) with the dim-0 halo
-    ("2d-vlasov-chunk-P2", _vlasov(1, 1, 1, [1040, 4]), 2, None),
-    ("3d-vlasov-chunk-P2", _vlasov(1, 2, 3, [140, 2, 2]), 2, None),
+    ("2d-vlasov-chunk-P2", _vlasov(1, 1, 1, [1040, 4]), 2, None, None),
+    ("3d-vlasov-chunk-P2", _vlasov(1, 2, 3, [140, 2, 2]), 2, None, None),
+    # checkerboard x-v partitions (NEXT-4): v dims split too, halo along v dims
+    ("4d-vlasov-P4-xv", _vlasov(2, 2, 3, [4, 6, 2, 4], extra=0.1), 4, [2, 1], [1, 2]),
+    ("5d-vlasov-P4-v", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 4, [1, 1, 1], [2, 2]),
+    ("5d-vlasov-P4-xv", _vlasov(3, 2, 3, [6, 6, 6, 4, 4]), 4, [1, 1, 2], [2, 1]),
+    ("6d-vlasov-P8-xv", _vlasov(3, 3, 3, [4, 4, 4, 2, 2, 2]), 8, [1, 2, 1], [2, 1, 2]),
 ]
 
 
@@ -72,8 +79,8 @@ def _join(spec, parts, meshes):
     return out.reshape(-1)
 
 
-@pytest.mark.parametrize("name,spec,P,xparts", CASES, ids=[c[0] for c in CASES])
-def test_partitioned_equals_single_rank_bitwise(name, spec, P, xparts):
+@pytest.mark.parametrize("name,spec,P,xparts,vparts", CASES, ids=[c[0] for c in CASES])
+def test_partitioned_equals_single_rank_bitwise(name, spec, P, xparts, vparts):
     import torch
     u = np.random.default_rng(11).uniform(-1, 1, configs.dof_count(spec))
     one = Mesh(spec)
@@ -86,7 +93,7 @@ def test_partitioned_equals_single_rank_bitwise(name, spec, P, xparts):
     sol = one.rk_step(bufs, 0, 0.0, dt, 3)
     ref_rk = bufs[sol].cpu().numpy()
 
-    meshes = [Mesh(spec, rank=r, nranks=P, xparts=xparts) for r in range(P)]
+    meshes = [Mesh(spec, rank=r, nranks=P, xparts=xparts, vparts=vparts) for r in range(P)]
     assert sum(m.owned_dofs for m in meshes) == u.size
     parts = _split(spec, u, meshes)
     us = [torch.from_numpy(p).cuda() for p in parts]

@@ -36,13 +36,18 @@ def _vlasov(d_x, d_v, cells, k=1):
     return _spec(d_x, d_v, k, cells, lo, hi, ac, lin)
 
 
+# (name, spec, P, xparts, vparts): automatic x partitions, explicit x-blocks, and checkerboard x-v
+# partitions that also split v dims (NEXT-4)
 CASES = [
-    ("3d-const-P2", _spec(2, 1, 2, [4, 6, 3], [0] * 3, [1] * 3, [1.0, -0.7, 0.3]), 2, None),
-    ("4d-vlasov-P2", _vlasov(2, 2, [4, 6, 2, 4]), 2, None),
-    ("4d-vlasov-P4", _vlasov(2, 2, [4, 6, 2, 4]), 4, None),
-    ("5d-vlasov-P8", _vlasov(3, 2, [4, 4, 6, 2, 2]), 8, None),
-    ("5d-vlasov-P4-x0split", _vlasov(3, 2, [4, 4, 6, 2, 2]), 4, [4, 1, 1]),
-    ("6d-vlasov-P8", _vlasov(3, 3, [2, 2, 2, 2, 2, 2]), 8, None),
+    ("3d-const-P2", _spec(2, 1, 2, [4, 6, 3], [0] * 3, [1] * 3, [1.0, -0.7, 0.3]), 2, None, None),
+    ("4d-vlasov-P2", _vlasov(2, 2, [4, 6, 2, 4]), 2, None, None),
+    ("4d-vlasov-P4", _vlasov(2, 2, [4, 6, 2, 4]), 4, None, None),
+    ("5d-vlasov-P8", _vlasov(3, 2, [4, 4, 6, 2, 2]), 8, None, None),
+    ("5d-vlasov-P4-x0split", _vlasov(3, 2, [4, 4, 6, 2, 2]), 4, [4, 1, 1], None),
+    ("6d-vlasov-P8", _vlasov(3, 3, [2, 2, 2, 2, 2, 2]), 8, None, None),
+    ("4d-vlasov-P4-xv", _vlasov(2, 2, [4, 6, 2, 4]), 4, [2, 1], [1, 2]),
+    ("5d-vlasov-P4-v", _vlasov(3, 2, [4, 4, 6, 2, 2]), 4, [1, 1, 1], [2, 2]),
+    ("6d-vlasov-P8-xv", _vlasov(3, 3, [2, 2, 2, 2, 2, 2]), 8, [1, 1, 2], [2, 2, 1]),
 ]
 
 
@@ -54,11 +59,11 @@ def _sign(spec, i, c):
     return 1 if a < 0 else 0
 
 
-def _owner_map(spec, P, xparts):
+def _owner_map(spec, P, xparts, vparts=None):
     d = spec["d_x"] + spec["d_v"]
     owner = -np.ones(spec["cells"][::-1], dtype=np.int64).transpose()  # index [c0, c1, ...]
     for r in range(P):
-        _, off, ln = partition_info(spec, r, P, xparts)
+        _, off, ln = partition_info(spec, r, P, xparts, vparts)
         sl = tuple(slice(off[i], off[i] + ln[i]) for i in range(d))
         assert np.all(owner[sl] == -1), "cells owned twice"
         owner[sl] = r
@@ -74,18 +79,20 @@ def _gid(spec, c):
     return g
 
 
-@pytest.mark.parametrize("name,spec,P,xparts", CASES, ids=[c[0] for c in CASES])
-def test_partition_covers_and_halo_is_the_remote_upwind_set(name, spec, P, xparts):
+@pytest.mark.parametrize("name,spec,P,xparts,vparts", CASES, ids=[c[0] for c in CASES])
+def test_partition_covers_and_halo_is_the_remote_upwind_set(name, spec, P, xparts, vparts):
     d, d_x = spec["d_x"] + spec["d_v"], spec["d_x"]
-    owner = _owner_map(spec, P, xparts)
-    xp, off, ln = partition_info(spec, 0, P, xparts)
-    assert int(np.prod(xp)) == P
+    owner = _owner_map(spec, P, xparts, vparts)
+    xp, off, ln = partition_info(spec, 0, P, xparts, vparts)
+    parts = [spec["cells"][i] // ln[i] for i in range(d)]
+    assert int(np.prod(parts)) == P
     for i in range(d_x, d):
-        assert ln[i] == spec["cells"][i], "v dims must not be split"
+        want = 1 if vparts is None else vparts[i - d_x]
+        assert parts[i] == want, "v dims are split exactly as requested"
     # independent: (cell, dim) pairs whose upwind neighbour is remote, per receiving rank
     expect = {r: set() for r in range(P)}
     for c in itertools.product(*[range(n) for n in spec["cells"]]):
-        for i in range(d_x):
+        for i in range(d):
             up = 1 if _sign(spec, i, c) else -1
             cn = list(c)
             cn[i] = (c[i] + up) % spec["cells"][i]
@@ -93,9 +100,9 @@ def test_partition_covers_and_halo_is_the_remote_upwind_set(name, spec, P, xpart
                 expect[owner[c]].add((_gid(spec, c), i, owner[tuple(cn)]))
     for r in range(P):
         got = set()
-        for i in range(d_x):
+        for i in range(d):
             for which in (2, 3):
-                peer, ids = halo_list(spec, r, P, i, which, xparts)
+                peer, ids = halo_list(spec, r, P, i, which, xparts, vparts)
                 assert len(ids) == len(set(ids))
                 got |= {(g, i, peer) for g in ids}
         assert got == expect[r], f"rank {r}: halo receive set differs from the remote-upwind set"
@@ -116,20 +123,21 @@ def _gloo_worker(rank, world, port, cases, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         errors = []
-        for name, spec, P, xparts in cases:
+        for name, spec, P, xparts, vparts in cases:
+            d = spec["d_x"] + spec["d_v"]
             # this process plays ranks rank, rank + world, ... of the P-rank partition
             mine = {}
             for r in range(rank, P, world):
-                for i in range(spec["d_x"]):
+                for i in range(d):
                     for which in range(4):
-                        mine[(r, i, which)] = halo_list(spec, r, P, i, which, xparts)
+                        mine[(r, i, which)] = halo_list(spec, r, P, i, which, xparts, vparts)
             allp = [None] * world
             dist.all_gather_object(allp, mine)
             plan = {}
             for part in allp:
                 plan.update(part)
             for r in range(rank, P, world):
-                for i in range(spec["d_x"]):
+                for i in range(d):
                     # what r receives from its left (which 2) is what the left rank sends right (which 1)
                     for recv_w, send_w in ((2, 1), (3, 0)):
                         peer, rids = plan[(r, i, recv_w)]
@@ -174,9 +182,10 @@ def test_config_partitions():
 
 # ---- the v-chunk pipeline: real per-chunk messages between gloo processes
 CHUNK_CASES = [
-    ("5d-pencil-P2-slab", _vlasov(3, 2, [6, 4, 4, 4, 4], k=3), 2, [1, 1, 2]),
-    ("6d-pencil-P2", _vlasov(3, 3, [2, 2, 4, 2, 2, 4], k=3), 2, None),
-    ("5d-pencil-P4-xblocks", _vlasov(3, 2, [6, 4, 4, 4, 4], k=3), 4, [1, 2, 2]),
+    ("5d-pencil-P2-slab", _vlasov(3, 2, [6, 4, 4, 4, 4], k=3), 2, [1, 1, 2], None),
+    ("6d-pencil-P2", _vlasov(3, 3, [2, 2, 4, 2, 2, 4], k=3), 2, None, None),
+    ("5d-pencil-P4-xblocks", _vlasov(3, 2, [6, 4, 4, 4, 4], k=3), 4, [1, 2, 2], None),
+    ("5d-pencil-P4-xv", _vlasov(3, 2, [6, 4, 4, 4, 4], k=3), 4, [1, 1, 2], [2, 1]),
 ]
 
 
@@ -193,33 +202,34 @@ def _chunk_worker(rank, world, port, case, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     errors = []
     try:
-        name, spec, P, xparts = case
-        units, chunks = halo_chunks(spec, rank, P, xparts)
+        name, spec, P, xparts, vparts = case
+        d = spec["d_x"] + spec["d_v"]
+        units, chunks = halo_chunks(spec, rank, P, xparts, vparts)
         if len(chunks) < 2:
             errors.append(f"{name}: expected several chunks, got {len(chunks)}")
         lists = {}
-        for i in range(spec["d_x"]):
+        for i in range(d):
             for which in range(4):
-                lists[(i, which)] = halo_list(spec, rank, P, i, which, xparts)
-        nleft = {i: len(lists[(i, 2)][1]) for i in range(spec["d_x"])}
-        covered_r = {i: [] for i in range(spec["d_x"])}
-        covered_l = {i: [] for i in range(spec["d_x"])}
+                lists[(i, which)] = halo_list(spec, rank, P, i, which, xparts, vparts)
+        nleft = {i: len(lists[(i, 2)][1]) for i in range(d)}
+        covered_r = {i: [] for i in range(d)}
+        covered_l = {i: [] for i in range(d)}
         for c, plan in enumerate(chunks):
             reqs, checks = [], []
-            for i in range(spec["d_x"]):
+            for i in range(d):
                 pr, to_right = lists[(i, 1)]
                 pl, to_left = lists[(i, 0)]
                 if pr < 0:
                     continue
-                d = plan[i]
-                (r0, nr), (l0, nl) = d["sr"], d["sl"]
+                pi = plan[i]
+                (r0, nr), (l0, nl) = pi["sr"], pi["sl"]
                 sr = torch.tensor(to_right[r0:r0 + nr], dtype=torch.int64)
                 sl = torch.tensor(to_left[l0:l0 + nl], dtype=torch.int64)
                 covered_r[i] += list(range(r0, r0 + nr))
                 covered_l[i] += list(range(l0, l0 + nl))
                 _, from_left = lists[(i, 2)]
                 _, from_right = lists[(i, 3)]
-                (a, na), (b, nb) = d["rl"], d["rr"]
+                (a, na), (b, nb) = pi["rl"], pi["rr"]
                 exp_l = from_left[a:a + na]
                 exp_r = from_right[b - nleft[i]:b - nleft[i] + nb]
                 rl = torch.empty(na, dtype=torch.int64)
@@ -239,7 +249,7 @@ def _chunk_worker(rank, world, port, case, q):
             for i, rl, exp_l, rr, exp_r in checks:
                 if rl.tolist() != list(exp_l) or rr.tolist() != list(exp_r):
                     errors.append(f"{name}: rank {rank} chunk {c} dim {i}: received ids differ")
-        for i in range(spec["d_x"]):
+        for i in range(d):
             if lists[(i, 1)][0] >= 0 and (sorted(covered_r[i]) != list(range(len(lists[(i, 1)][1]))) or
                                           sorted(covered_l[i]) != list(range(len(lists[(i, 0)][1])))):
                 errors.append(f"{name}: rank {rank} dim {i}: the chunks do not partition the send lists")
