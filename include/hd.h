@@ -5,7 +5,7 @@
  *
  * What the library computes (FP64, periodic Cartesian box T = T_x (x) T_v; nodal
  * Lagrange basis on the n = k+1 Gauss-Legendre points of each 1D reference interval [0,1],
- * reading C1; upwind numerical flux, reading C3):
+ * reading C1; upwind numerical flux, or the central flux on single-rank meshes, reading C3):
  *   hd_apply_advection  v <- A(u), the DG weak form of Eq. into:adv:ref,
  *                       A(u)_i = (grad phi_i, a u)_cell - sum_faces <phi_i, (a.n) u_up>_face
  *                       (sign convention P:236, reading C4; output is the weak form, C5).
@@ -62,8 +62,12 @@ typedef struct {
   double lo[6], hi[6];  /* box per dim, hi > lo; periodic in every dim (C9) */
   double a_const[6];    /* advection field a_i(z) = a_const[i] + sum_j a_lin[i][j] z_j ...   */
   double a_lin[36];     /* ... row-major [i][j]; a_lin[i][i] must be 0 (divergence free); the
-                           sign of a_i must be constant on every cell (reading C11) */
-  int flux;             /* 0 = upwind (the only flux built on the GPU path) */
+                           sign of a_i must be constant on every cell with the upwind flux
+                           (reading C11; HD_ERR_UNSUPPORTED otherwise) */
+  int flux;             /* 0 = upwind; 1 = central, F* = (a.n)(u- + u+)/2, nranks = 1 only
+                           (HD_ERR_UNSUPPORTED otherwise); evaluated as the mean of the two one-sided
+                           operators (every face taking its left cell's trace, resp. its right cell's),
+                           i.e. two cell-kernel launches per application or RK stage */
   int rank, nranks;     /* phase-space partition over nranks ranks: the ranks form a grid
                            parts[0] x .. x parts[d-1] over the cells (parts = xparts, then vparts); rank r
                            has block coordinates b_i = (r / prod_{j<i} parts_j) % parts_i */

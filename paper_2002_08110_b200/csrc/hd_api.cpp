@@ -154,6 +154,8 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
 // dt for an RK stage): s_i K[s], s_i tau[s], s_i = a_i dtfac / h_i, compact [dim][sign][N][N] / [N]. The
 // line speed is formed exactly as the kernel's line_speed does for a constant field ((a_i + 0) * fac).
 void set_dtfac(hd_mesh *m, hd::CellParams &p, double dtfac) {
+  // central flux: each of the two one-sided operators enters with weight 1/2
+  if (m->desc.flux == 1) dtfac *= 0.5;
   p.dtfac = dtfac;
   const int N = m->n;
   for (int i = 0; i < m->d; ++i) {
@@ -192,6 +194,8 @@ void free_mesh(hd_mesh *m) {
     if (m->tbuf[i]) cudaFree(m->tbuf[i]);
   if (m->flags) cudaFree(m->flags);
   if (m->sched) cudaFree(m->sched);
+  if (m->sched2) cudaFree(m->sched2);
+  if (m->schedc2) cudaFree(m->schedc2);
   if (m->dbg) cudaFree(m->dbg);
   if (m->schedc) cudaFree(m->schedc);
   for (int i = 0; i < 6; ++i) {
@@ -237,8 +241,8 @@ hd_status plan_traces(hd_mesh *m) {
     m->follow[i] = 0;
     m->tbuf[i] = nullptr;
     if (i == 0 || !g.pencil || m->pt.len[i] < 2) continue;
-    bool follow = true;
-    for (int j = 0; j < i; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
+    bool follow = true;  // (central flux: the forced sides are constant, every dim follows)
+    for (int j = 0; j < i && m->desc.flux == 0; ++j) follow = follow && m->desc.a_lin[6 * i + j] == 0.0;
     m->follow[i] = follow ? 1 : 0;
     if (!follow || !use) continue;
     m->pub[i] = 1;
@@ -266,7 +270,10 @@ hd_status plan_traces(hd_mesh *m) {
   m->epoch = 0;
   // skew (steps a same-round producer runs ahead of its consumer): 2 gives the producer a full step of
   // margin; the first `skew` steps of a pencil then read their upwind neighbours directly
-  m->skew = g.pencil && g.GPU > 2 ? 2 : (g.pencil && g.GPU > 1 ? 1 : 0);
+#ifndef HD_SKEW
+#define HD_SKEW 2
+#endif
+  m->skew = g.pencil && g.GPU > HD_SKEW ? HD_SKEW : (g.pencil && g.GPU > 1 ? 1 : 0);
   return HD_OK;
 }
 
@@ -275,9 +282,15 @@ hd_status plan_traces(hd_mesh *m) {
 hd_status upload_schedule(hd_mesh *m) {
   std::vector<hd::SchedDim> recs;
   std::vector<hd::SchedCell> cells;
-  hd::build_schedule(*m, recs, cells);
+  const bool central = m->desc.flux == 1;
+  hd::build_schedule(*m, recs, cells, central ? 0 : -1);
   hd_status st = upload(&m->sched, recs.data(), recs.size(), "schedule");
   if (st == HD_OK) st = upload(&m->schedc, cells.data(), cells.size(), "schedule");
+  if (st == HD_OK && central) {
+    hd::build_schedule(*m, recs, cells, 1);
+    st = upload(&m->sched2, recs.data(), recs.size(), "schedule");
+    if (st == HD_OK) st = upload(&m->schedc2, cells.data(), cells.size(), "schedule");
+  }
   return st;
 }
 
@@ -504,7 +517,9 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   long long nd = 1;
   for (int i = 0; i < d; ++i) nd *= n;
   if (n > 64 || ncells > (1LL << 62) / nd) return fail(HD_ERR_ARG, "DoF count overflows 64-bit indexing");
-  if (desc->flux != 0) return fail(HD_ERR_UNSUPPORTED, "only the upwind flux (0) is built on the GPU path");
+  if (desc->flux != 0 && desc->flux != 1) return fail(HD_ERR_ARG, "flux must be 0 (upwind) or 1 (central)");
+  if (desc->flux == 1 && desc->nranks > 1)
+    return fail(HD_ERR_UNSUPPORTED, "the central flux is built for single-rank meshes only");
   if (n < 2 || n > 6 || !hd::cell_kernel_supported(d, n))
     return fail(HD_ERR_UNSUPPORTED, "(d=%d, n=%d) is not in the built kernel set", d, n);
   if (desc->nranks < 1 || desc->rank < 0 || desc->rank >= desc->nranks)
@@ -516,7 +531,7 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   }
   // the sign of each a_i must be constant on every cell (reading C11): check the affine field's
   // range over each 1D cell slab of the dims it depends on
-  for (int i = 0; i < d; ++i) {
+  for (int i = 0; i < d && desc->flux == 0; ++i) {  // (the central flux never selects a side)
     bool any_lin = false;
     for (int j = 0; j < d; ++j) any_lin |= desc->a_lin[6 * i + j] != 0.0;
     if (!any_lin) continue;
@@ -602,7 +617,7 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   }
   {
     // pencil mode needs one dim-0 direction per group: a_0 must not depend on z_1
-    const int pencil_ok = d < 2 || m->desc.a_lin[6 * 0 + 1] == 0.0;
+    const int pencil_ok = d < 2 || m->desc.a_lin[6 * 0 + 1] == 0.0 || m->desc.flux == 1;
     m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, pencil_ok);
   }
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / (pt.len[0] * m->geo.CT) : m->ncells_local / m->geo.CT);
@@ -909,6 +924,31 @@ hd_status launch_units(hd_mesh *m, hd::CellParams &p, int u0, int u1, cudaStream
 // chunk c's traces have arrived -- so the exchange of chunk c+1 overlaps the cell kernel of chunk c.
 hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU, double *out, int mode, double a,
                        double b, cudaStream_t s) {
+  if (m->desc.flux == 1) {
+    // central flux: F* = (a.n)(u- + u+)/2 is the mean of the two one-sided operators (every face taking
+    // its left cell's trace, resp. its right cell's), each evaluated with the signed speed and weight 1/2
+    // (set_dtfac). A mode: v = A_left u / 2, then v += A_right u / 2. RK stage: dU <- A_s dU + dt/2 M^-1
+    // A_left U (no U' store), then dU <- dU + dt/2 M^-1 A_right U and U' <- U + B_s dU.
+    hd_status st = begin_stage(m, p, U, dU, out, mode, a, b, s);
+    if (st != HD_OK) return st;
+    p.sched = m->sched;
+    p.schedc = m->schedc;
+    p.acc_out = 0;
+    p.skip_u = mode != hd::kModeAdvection;
+    st = launch_units(m, p, 0, m->nunits, s);
+    if (st == HD_OK) st = begin_stage(m, p, U, dU, out, mode == hd::kModeAdvection ? mode : hd::kModeRK,
+                                      mode == hd::kModeAdvection ? 0.0 : 1.0, b, s);
+    if (st != HD_OK) return st;
+    p.sched = m->sched2;
+    p.schedc = m->schedc2;
+    p.acc_out = mode == hd::kModeAdvection;
+    p.skip_u = 0;
+    st = launch_units(m, p, 0, m->nunits, s);
+    p.sched = m->sched;
+    p.schedc = m->schedc;
+    p.acc_out = 0;
+    return st;
+  }
   hd_status st = begin_stage(m, p, U, dU, out, mode, a, b, s);
   if (st != HD_OK) return st;
   if (m->desc.nranks == 1) return launch_units(m, p, 0, m->nunits, s);

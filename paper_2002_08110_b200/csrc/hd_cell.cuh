@@ -614,7 +614,11 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
-      for (int b = 0; b < N; ++b) __stcs(p.out + g0 + a * SP + b * SQ, acc[a][b] * (wr * (T.w[a] * T.w[b])));
+      for (int b = 0; b < N; ++b) {
+        double v = acc[a][b] * (wr * (T.w[a] * T.w[b]));
+        if (p.acc_out) v += __ldcs(p.out + g0 + a * SP + b * SQ);  // central flux: second one-sided half
+        __stcs(p.out + g0 + a * SP + b * SQ, v);
+      }
   } else {
     // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU. U is still in uv; dU arrived
     // (cp.async issued by stage_du) in this thread's own slots of the accumulator buffer.
@@ -630,7 +634,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         __stcs(p.du + g0 + a * SP + b * SQ, acc[a][b]);
-        __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], uv[a][b]));
+        if (!p.skip_u) __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], uv[a][b]));
       }
   }
 }

@@ -100,6 +100,8 @@ struct CellParams {
   int FN;                 // n^(d-1): doubles per trace
   int prefetch;           // bulk-prefetch cells that will be read directly into L2
   long long cstride;      // cell-index stride between the cells of a group (pencil mode: L_0; else 1)
+  int acc_out;            // A mode: out += the result (second half of a central-flux application)
+  int skip_u;             // RK mode: dU only, no U' store (first half of a central-flux stage)
   const SchedDim *sched;  // [nunits * GPU][CT][D]
   const SchedCell *schedc;  // [nunits * GPU][CT]
   int *flags;             // [nunits rounded up to 4] unit progress flags
@@ -169,7 +171,8 @@ cudaError_t launch_finite_check(const double *v, long long n, int *err, cudaStre
 bool cell_kernel_supported(int d, int n);
 
 // Static schedule of a mesh (hd_sched.cpp): [nunits * GPU][CT][d] records (see SchedDim).
-void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<SchedCell> &cells);
+// forced = -1: upwind by the sign of a_i; 0 / 1: every dim takes its left / right neighbour (central flux)
+void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<SchedCell> &cells, int forced);
 // Kernel geometry for (d, n) on a local box with L0 cells along dim 0 and ncells cells: cells per group
 // CT, pencil mode, threads per CTA, dynamic smem bytes, phases.
 struct CellGeometry {
@@ -205,8 +208,10 @@ struct hd_mesh {
   double *tbuf[6];
   int *flags;
   long long nflags;        // flag words allocated (nunits rounded up to 4)
-  hd::SchedDim *sched;     // device copy of the static schedule
+  hd::SchedDim *sched;     // device copy of the static schedule (central flux: the left-neighbour one)
   hd::SchedCell *schedc;
+  hd::SchedDim *sched2;    // central flux: the right-neighbour schedule
+  hd::SchedCell *schedc2;
   long long epoch;
   int grid;
   // halo (nranks > 1): per x dim receive buffer and slot table; one send buffer for all dims, laid

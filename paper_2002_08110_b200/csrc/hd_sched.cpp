@@ -3,6 +3,10 @@
 // lane per (cell, dim), divergent, ~20 instructions per DoF); the decisions are all static, so they are
 // made here and stored as one 32-byte SchedDim record per (group, cell slot, dim).
 //
+// Central flux (NEXT-3): the schedule can force every dim's "upwind" side (forced = 0: the left neighbour,
+// 1: the right one) -- the two one-sided operators whose mean is the central-flux operator;
+// the traversal then follows the forced direction.
+//
 // Work decomposition (unchanged from round 1):
 //   * pencil mode (CT | L_1, a_0 independent of z_1): a group is CT cells at one c_0 from CT adjacent
 //     dim-0 pencils; a unit is those CT pencils, processed by ONE CTA group by group, upwind -> downwind
@@ -26,6 +30,7 @@ namespace {
 
 struct Geo {
   int d, CT, GPU, pencil, skew;
+  int forced;  // -1: the sign of a_i decides the upwind side; 0 / 1: every dim takes its left / right neighbour
   long long L[kMaxD], lstride[kMaxD], ustride[kMaxD], off[kMaxD];
   int follow[kMaxD], pub[kMaxD], xsplit[kMaxD];
   long long UC;
@@ -43,7 +48,7 @@ void cell_speed(const Geo &g, int i, const long long *c, double &base, int &sg) 
     half = std::fma(ds.a_lin[6 * i + j], 0.5 * g.m->h[j], half);
   }
   base = ab;
-  sg = (ab + half) < 0.0 ? 1 : 0;
+  sg = g.forced >= 0 ? g.forced : (ab + half) < 0.0 ? 1 : 0;
 }
 
 struct Unit {
@@ -136,9 +141,10 @@ void decode_unit(const Geo &g, long long u, Unit &ui) {
 
 }  // namespace
 
-void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<SchedCell> &cells) {
+void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<SchedCell> &cells, int forced) {
   Geo g{};
   g.m = &m;
+  g.forced = forced;
   g.d = m.d;
   g.CT = m.geo.CT;
   g.GPU = m.geo.GPU;

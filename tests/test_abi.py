@@ -65,8 +65,12 @@ def test_invalid_descriptors_are_rejected_on_host(lib):
     assert st == -1 and "d_x" in msg
     assert _create(lib, _spec(), rank=2, nranks=2)[0] == -1
     assert _create(lib, _spec(), rank=0, nranks=3)[0] == -1                 # 3 does not divide |C_x| = 4
-    # valid but unsupported: central flux, k = 0, v = 0 inside a cell
-    assert _create(lib, _spec(flux="central"))[0] == -2
+    # valid but unsupported: central flux across ranks, k = 0, v = 0 inside a cell (upwind only, C11)
+    # (a valid single-rank central mesh passes host validation: HD_OK on a GPU box, HD_ERR_CUDA here)
+    assert _create(lib, _spec(flux="central"))[0] in (0, -3)
+    assert _create(lib, _spec(flux="central"), rank=0, nranks=2)[0] == -2
+    assert _create(lib, _spec(lo=[0, -1], hi=[1, 1], cells=[4, 3], a_const=[0.0, 0.3], a_lin=[[0, 1.0], [0, 0]],
+                              flux="central"))[0] in (0, -3)
     assert _create(lib, _spec(k=0))[0] == -2
     st, msg = _create(lib, _spec(lo=[0, -1], hi=[1, 1], cells=[4, 3], a_const=[0.0, 0.3],
                                  a_lin=[[0, 1.0], [0, 0]]))

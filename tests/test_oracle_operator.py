@@ -130,6 +130,19 @@ def _traces(spec, u):
     return U, x, w, l0, l1, shape
 
 
+def test_central_flux_is_skew():
+    # with F* = (a.n)(u- + u+)/2 and div a = 0 the face terms cancel the volume term's boundary part:
+    # u^T A_c(u) = 0 for every u (energy conservation of the semi-discrete central scheme); a one-sided
+    # trace, a dropped face term or a wrong sign would leave the -1/2 sum |a.n| (u- - u+)^2 jump term
+    for vlasov in (False, True):
+        spec = dict(tiny_spec(3, 2, vlasov), flux="central")
+        N = capi.dof_count(spec)
+        for seed in (4, 5):
+            u = np.random.default_rng(seed).uniform(-1, 1, N)
+            v = capi.apply_advection(spec, u)
+            assert abs(u @ v) <= 1e-13 * np.linalg.norm(u) * np.linalg.norm(v), (vlasov, u @ v)
+
+
 def test_upwind_energy_identity():
     # u^T A(u) = -1/2 sum_faces sum_q w_f |J_f| |a.n| (u- - u+)^2 (exact for div a = 0)
     for vlasov in (False, True):

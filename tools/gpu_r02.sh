@@ -27,10 +27,10 @@ for c in 6d 5d; do
   done
 done
 # full captures
-for spec in "6d rk" "6d adv" "5d rk"; do
+for spec in "6d rk 6" "6d adv 2" "5d rk 6"; do
   set -- $spec
-  c=$1; op=$2; tag=full_${c}_$op
-  timeout 1500 ncu --set full --import-source on --clock-control none -k regex:cell_kernel -s 6 -c 1 \
+  c=$1; op=$2; skip=$3; tag=full_${c}_$op
+  timeout 1500 ncu --set full --import-source on --clock-control none -k regex:cell_kernel -s $skip -c 1 \
      -o $O/ncu_$tag python tools/prof_driver.py --config $c --op $op --reps 3 > $O/ncu_$tag.log 2>&1
   python tools/ncu_summary.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_$tag.txt 2>&1
   python tools/ncu_lines.py $O/ncu_$tag.ncu-rep 40 > $O/ncu_${tag}_lines.txt 2>&1
