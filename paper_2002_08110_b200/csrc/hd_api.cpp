@@ -927,26 +927,21 @@ hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *d
   if (m->desc.flux == 1) {
     // central flux: F* = (a.n)(u- + u+)/2 is the mean of the two one-sided operators (every face taking
     // its left cell's trace, resp. its right cell's), each evaluated with the signed speed and weight 1/2
-    // (set_dtfac). A mode: v = A_left u / 2, then v += A_right u / 2. RK stage: dU <- A_s dU + dt/2 M^-1
-    // A_left U (no U' store), then dU <- dU + dt/2 M^-1 A_right U and U' <- U + B_s dU.
+    // (set_dtfac). A mode: v = A_left u / 2, then (kModeAdvAcc) v += A_right u / 2. RK stage: dU <- A_s dU +
+    // dt/2 M^-1 A_left U (its U' store is provisional), then dU <- dU + dt/2 M^-1 A_right U, U' <- U + B_s dU.
     hd_status st = begin_stage(m, p, U, dU, out, mode, a, b, s);
     if (st != HD_OK) return st;
     p.sched = m->sched;
     p.schedc = m->schedc;
-    p.acc_out = 0;
-    p.skip_u = mode != hd::kModeAdvection;
     st = launch_units(m, p, 0, m->nunits, s);
-    if (st == HD_OK) st = begin_stage(m, p, U, dU, out, mode == hd::kModeAdvection ? mode : hd::kModeRK,
+    if (st == HD_OK) st = begin_stage(m, p, U, dU, out, mode == hd::kModeAdvection ? hd::kModeAdvAcc : hd::kModeRK,
                                       mode == hd::kModeAdvection ? 0.0 : 1.0, b, s);
     if (st != HD_OK) return st;
     p.sched = m->sched2;
     p.schedc = m->schedc2;
-    p.acc_out = mode == hd::kModeAdvection;
-    p.skip_u = 0;
     st = launch_units(m, p, 0, m->nunits, s);
     p.sched = m->sched;
     p.schedc = m->schedc;
-    p.acc_out = 0;
     return st;
   }
   hd_status st = begin_stage(m, p, U, dU, out, mode, a, b, s);

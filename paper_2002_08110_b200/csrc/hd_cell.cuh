@@ -421,7 +421,7 @@ template <int D, int N, int MODE, int PH>
 __device__ __forceinline__ void phase_entry(const CellParams &p, int r, double *ptab) {
   using G = CGeo<D, N>;
   ThreadPhase tp;
-  thread_phase<D, N, PH, PH == G::NPH - 1 && MODE == kModeAdvection>(p, r, tp);
+  thread_phase<D, N, PH, PH == G::NPH - 1 && (MODE == kModeAdvection || MODE == kModeAdvAcc)>(p, r, tp);
   double *pt = ptab + PH * 1024;
   const int tid = (int)threadIdx.x;
   pt[tid] = tp.wP;
@@ -608,15 +608,16 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) gb.A[sidx<D, N>(sR, a * SP + b * SQ)] = acc[a][b];
-  } else if constexpr (MODE == kModeAdvection) {
-    // weak form: v = M (M^-1 A u), M_qq = |J| prod_i w_{q_i}
+  } else if constexpr (MODE == kModeAdvection || MODE == kModeAdvAcc) {
+    // weak form: v = M (M^-1 A u), M_qq = |J| prod_i w_{q_i}; kModeAdvAcc (second one-sided half of a
+    // central-flux application) adds to v
     const double wr = ptab[PH * 1024 + 512 + tid];
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         double v = acc[a][b] * (wr * (T.w[a] * T.w[b]));
-        if (p.acc_out) v += __ldcs(p.out + g0 + a * SP + b * SQ);  // central flux: second one-sided half
+        if constexpr (MODE == kModeAdvAcc) v += __ldcs(p.out + g0 + a * SP + b * SQ);
         __stcs(p.out + g0 + a * SP + b * SQ, v);
       }
   } else {
@@ -634,7 +635,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         __stcs(p.du + g0 + a * SP + b * SQ, acc[a][b]);
-        if (!p.skip_u) __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], uv[a][b]));
+        __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], uv[a][b]));
       }
   }
 }

@@ -31,7 +31,7 @@ struct Tables1D {
 // Host-side computation of the tables (independent of the oracle).
 void build_tables(int n, Tables1D &t);
 
-enum Mode : int { kModeAdvection = 0, kModeRK = 1, kModeRKFirst = 2 };
+enum Mode : int { kModeAdvection = 0, kModeRK = 1, kModeRKFirst = 2, kModeAdvAcc = 3 /* v += A u (central flux) */ };
 
 // x-space partition of the ranks (hd_plan.cpp)
 struct Partition {
@@ -100,8 +100,6 @@ struct CellParams {
   int FN;                 // n^(d-1): doubles per trace
   int prefetch;           // bulk-prefetch cells that will be read directly into L2
   long long cstride;      // cell-index stride between the cells of a group (pencil mode: L_0; else 1)
-  int acc_out;            // A mode: out += the result (second half of a central-flux application)
-  int skip_u;             // RK mode: dU only, no U' store (first half of a central-flux stage)
   const SchedDim *sched;  // [nunits * GPU][CT][D]
   const SchedCell *schedc;  // [nunits * GPU][CT]
   int *flags;             // [nunits rounded up to 4] unit progress flags

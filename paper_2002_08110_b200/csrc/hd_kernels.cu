@@ -313,6 +313,7 @@ cudaError_t launch_cell_dn(const CellParams &p, cudaStream_t s, int grid_max) {
     switch (p.mode) {
       case kModeAdvection: return launch_cell_impl<D, N, kModeAdvection>(p, s, grid_max);
       case kModeRK: return launch_cell_impl<D, N, kModeRK>(p, s, grid_max);
+      case kModeAdvAcc: return launch_cell_impl<D, N, kModeAdvAcc>(p, s, grid_max);
       default: return launch_cell_impl<D, N, kModeRKFirst>(p, s, grid_max);
     }
   }
@@ -324,12 +325,14 @@ cudaError_t grid_dn(const CellGeometry &g, int sms, int *grid) {
     return cudaErrorNotSupported;
   } else {
     // all modes share the geometry; take the minimum co-residency over them
-    int g0 = 0, g1 = 0, g2 = 0;
+    int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
     cudaError_t e = grid_impl<D, N, kModeAdvection>(g, sms, &g0);
     if (e == cudaSuccess) e = grid_impl<D, N, kModeRK>(g, sms, &g1);
     if (e == cudaSuccess) e = grid_impl<D, N, kModeRKFirst>(g, sms, &g2);
+    if (e == cudaSuccess) e = grid_impl<D, N, kModeAdvAcc>(g, sms, &g3);
     int m = g0 < g1 ? g0 : g1;
-    *grid = m < g2 ? m : g2;
+    m = m < g2 ? m : g2;
+    *grid = m < g3 ? m : g3;
     return e;
   }
 }
