@@ -120,8 +120,14 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
 #ifdef HD_PROFILE
 #define HD_PROF_DECL                                                                  \
   unsigned long long pf_t = clock64(), pf_wait[4] = {0, 0, 0, 0}, pf_work[4] = {0, 0, 0, 0}, pf_groups = 0; \
-  unsigned long long pf_sub[3][6] = {};
+  unsigned long long pf_sub[3][6] = {}, pf_main[8] = {}, pf_m = 0;
 #define HD_PF(ph) pf_sub[ph]
+#define HD_MARK(k)                          \
+  do {                                      \
+    const unsigned long long t_ = clock64(); \
+    pf_main[(k)] += t_ - pf_m;              \
+    pf_m = t_;                              \
+  } while (0)
 #define HD_PROF_BAR(site)                                                              \
   do {                                                                                 \
     const unsigned long long ta_ = clock64();                                          \
@@ -130,6 +136,7 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
     const unsigned long long tb_ = clock64() + *(volatile int *)smem_raw * 0;          \
     pf_wait[site] += tb_ - ta_;                                                        \
     pf_t = tb_;                                                                        \
+    pf_m = tb_;                                                                        \
   } while (0)
 #define HD_PROF_GROUP() ++pf_groups
 #define HD_SUB_DECL unsigned long long sb_t = clock64();
@@ -151,8 +158,16 @@ __device__ __forceinline__ constexpr int sidx(int sR, int T) {
       printf("HDSUB warp %d phase %d | loads %llu passP %llu passQ %llu trP+liftP %llu trQ+liftQ %llu store %llu\n", \
              threadIdx.x >> 5, ph_, pf_sub[ph_][0] / pf_groups, pf_sub[ph_][1] / pf_groups,                     \
              pf_sub[ph_][2] / pf_groups, pf_sub[ph_][3] / pf_groups, pf_sub[ph_][4] / pf_groups,                \
-             pf_sub[ph_][5] / pf_groups)
+             pf_sub[ph_][5] / pf_groups);                                                               \
+  if ((blockIdx.x == 0) && (threadIdx.x & 31) == 0 && pf_groups)                                              \
+    printf("HDMAIN warp %d | stage %llu fetch %llu cells %llu ph0 %llu | flags %llu ph1 %llu | ph2 %llu resolve %llu\n", \
+           threadIdx.x >> 5, pf_main[0] / pf_groups, pf_main[1] / pf_groups, pf_main[2] / pf_groups,               \
+           pf_main[3] / pf_groups, pf_main[4] / pf_groups, pf_main[5] / pf_groups, pf_main[6] / pf_groups,        \
+           pf_main[7] / pf_groups)
 #else
+#define HD_MARK(k) \
+  do {             \
+  } while (0)
 #define HD_PROF_DECL
 #define HD_PF(ph) nullptr
 #define HD_PROF_BAR(site) __syncthreads()
@@ -638,6 +653,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
         __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], uv[a][b]));
       }
   }
+  HD_SUB(5);
 }
 
 // Shared-memory carve-up (offsets in doubles, every region 16-byte aligned):
@@ -862,6 +878,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     } else {
       for (int q = 0; q < NPH; ++q) cp_async_commit();
     }
+    HD_MARK(0);
     {
       int ua, ga;
       if (ahead(u, gi, kRing - 1, ua, ga)) fetch((it + kRing - 1) % kRing, (long long)ua * p.GPU + ga);
@@ -870,6 +887,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     if (MODE == kModeRK && tid == 0 && p.prefetch)
       for (int kc = 0; kc < CT; ++kc)
         prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
+    HD_MARK(1);
     auto flags_next = [&]() {
       if (has_next) {
         acquire(slot1);
@@ -885,6 +903,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     // the next group's cells stream into the other cell buffer (free since the previous group ended)
     if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs + (s ^ 1) * CND);
     cp_async_commit();
+    HD_MARK(2);
     auto refill = [&](int sR, int R) {
       // RK: dU of this thread's tile into its own (already read) accumulator slots
       if constexpr (MODE == kModeRK) {
@@ -909,17 +928,22 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       run_phase<D, N, MODE, 0, WLAST>(p, ci, ptab, stg, r, gb, active, refill);
     } else {
       run_phase<D, N, MODE, 0, NPH + 1>(p, ci, ptab, stg, r, gb, active, none, HD_PF(0));
+      HD_MARK(3);
       HD_PROF_BAR(1);
       flags_next();
+      HD_MARK(4);
       if constexpr (NPH == 2) {
         run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill);
       } else {
         run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 3>(p, ci, ptab, stg, r, gb, active, none, HD_PF(1));
+        HD_MARK(5);
         HD_PROF_BAR(2);
         run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill, HD_PF(2));
+        HD_MARK(6);
       }
     }
     if (has_next) resolve(slot1, info0 + (s ^ 1) * MAXCT);
+    HD_MARK(7);
     cp_async_wait<0>();  // the next group's cells (and the records fetched this group)
     prev_unit = p.flags ? u : -1;
     prev_step = gi;
