@@ -125,6 +125,7 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   p.sched = m->sched;
   p.schedc = m->schedc;
   p.flags = m->flags;
+  p.uctr = m->dbg + 32;
   p.dtfac = 1.0;
   p.err = m->dbg;
   p.stag = m->dbg + 1;
@@ -628,8 +629,9 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
   }
   st = plan_traces(m);
   if (st == HD_OK) {
-    cudaError_t e2 = cudaMalloc(&m->dbg, 32 * sizeof(int));
-    if (e2 == cudaSuccess) e2 = cudaMemset(m->dbg, 0, 32 * sizeof(int));
+    // [0..31] debug words (HD_DEBUG), [32] the unit counter of the cell kernel
+    cudaError_t e2 = cudaMalloc(&m->dbg, 64 * sizeof(int));
+    if (e2 == cudaSuccess) e2 = cudaMemset(m->dbg, 0, 64 * sizeof(int));
     if (e2 != cudaSuccess) st = cuda_fail(e2, "debug words");
   }
   m->nchunk = 1;
@@ -913,8 +915,20 @@ hd_status begin_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *dU
 hd_status launch_units(hd_mesh *m, hd::CellParams &p, int u0, int u1, cudaStream_t s) {
   p.u_begin = u0;
   p.u_end = u1;
-  cudaError_t e = hd::launch_cell_kernel(m->d, m->n, p, s, &m->launches, m->grid);
+  p.uctr = m->dbg + 32;
+  cudaError_t e = cudaMemsetAsync(p.uctr, 0, sizeof(int), s);
+  if (e != cudaSuccess) return cuda_fail(e, "unit counter");
+  e = hd::launch_cell_kernel(m->d, m->n, p, s, &m->launches, m->grid);
   if (e != cudaSuccess) return cuda_fail(e, "cell kernel");
+#ifdef HD_COUNT
+  {  // experiment builds: trace-source counts of this launch (ready published, late published, direct)
+    int c[4] = {0, 0, 0, 0};
+    cudaStreamSynchronize(s);
+    cudaMemcpy(c, m->dbg + 25, sizeof(c), cudaMemcpyDeviceToHost);
+    cudaMemset(m->dbg + 25, 0, sizeof(c));
+    fprintf(stderr, "HDCOUNT grid %d pub_ready %d pub_late %d direct %d\n", m->grid, c[0], c[1], c[2]);
+  }
+#endif
   return HD_OK;
 }
 

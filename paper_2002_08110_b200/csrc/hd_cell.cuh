@@ -19,11 +19,27 @@
 // neighbour (smem), a trace published by an earlier unit (global, ready when its producer's progress
 // flag -- read with ld.acquire -- says so), the halo buffer, or a direct read of the neighbour cell.
 #pragma once
-#ifndef HD_MINB
-#define HD_MINB 1
+// Lean kernel: two CTAs per SM -- two cell buffers (U, accumulator; the next group's cells
+// stream into U once every thread has read its last-phase tile), one dim-0 carry buffer, published / halo
+// traces read from L2 in the phase instead of staged, <= 128 registers per thread. Used for d >= 4 with
+// n <= 4 (the n = 5 tile does not fit 128 registers); HD_LEAN = 0 / 1 forces it off / on (experiments).
+#ifndef HD_LEAN
+#define HD_LEAN -1
+#endif
+#ifndef HD_LEAN_PF
+#define HD_LEAN_PF 1
+#endif
+#ifndef HD_DYN
+#define HD_DYN 1
 #endif
 
 namespace hd {
+
+template <int D, int N>
+__host__ __device__ constexpr bool lean() {
+  return HD_LEAN == 1 || (HD_LEAN < 0 && D >= 4 && N <= 4);
+}
+constexpr bool kDyn = HD_DYN != 0;
 
 // Shared-memory layout of a cell: element (d_0, ..., d_{D-1}) at sum_i d_i S_i -- ADDITIVE, so a thread's
 // tile element is its rest offset plus a compile-time constant (base + immediate addressing). The padded
@@ -468,13 +484,15 @@ template <int D, int N, int X, int SX, int SY>
 __device__ __forceinline__ void trace_in(const CellParams &p, const CellInfo &ci, int r, int sR, int R, const GroupBufs &gb,
                                          LineSpeed ls, const double *stg, double (&t)[N]) {
   using G = CGeo<D, N>;
+  constexpr bool kLean = lean<D, N>();
   switch (ci.src[X]) {
     case kSrcCarry:
       load_vec<N>(gb.carry + N * r, t, false);
       break;
     case kSrcPub:
     case kSrcHalo:
-      load_vec<N>(stg, t, false);
+      if constexpr (kLean) load_vec<N>(ci.tsrc[X] + N * r, t, true);
+      else load_vec<N>(stg, t, false);
       break;
     case kSrcGroup:
       trace_cell<D, N, X, SX, SY, true>(p, gb.Ugrp + (size_t)ci.nb[X] * G::NDP, sR, ls, ci.sg[X], p.var[X], t);
@@ -539,6 +557,7 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
                                           unsigned long long *pf_sub = nullptr) {
   HD_SUB_DECL
   using G = CGeo<D, N>;
+  constexpr bool kLean = lean<D, N>();
   constexpr int P = G::P(PH), Q = G::Q(PH);
   constexpr bool QA = G::QA(PH);
   constexpr int SP = ipow(N, P), SQ = ipow(N, Q);
@@ -572,36 +591,51 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
         for (int b = 0; b < N; ++b) uv[a][b] = gb.U[sidx<D, N>(sR, a * SP + b * SQ)];
     }
-    if constexpr (!FIRST) {
+    if constexpr (!FIRST && !kLean) {
 #pragma unroll
       for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int b = 0; b < N; ++b) acc[a][b] = gb.A[sidx<D, N>(sR, a * SP + b * SQ)];
     }
   }
-  if constexpr (LAST) refill(sR, R);  // RK: dU into this thread's own accumulator slots (read above)
-  if (!active) return;
-  const size_t g0 = (size_t)ci.cell * G::ND + R;
-  HD_SUB(0);
-
   // volume terms of P and Q and this cell's downwind traces along P and Q (stored right away)
-  {
-    double tr[N];
-    pass_P_any<N, P, FIRST>(p, acc, uv, lsP, tr, ci.sg[P], p.var[P]);
-    const unsigned char oP = ci.out[P];
-    if (oP == kOutCarry) store_vec<N>(gb.carry_out + N * r, tr, false);
-    else if (oP == kOutPub) store_vec<N>(p.tbuf[P] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
+  // lean: one carry buffer -- the incoming dim-0 carry (this thread's own slot) is read before the pass
+  // overwrites it with the outgoing one; the passes start a fresh accumulator (the earlier phases' sum is
+  // added after the lifts), so the tile and the old accumulator are never live together
+  constexpr bool EARLY = kLean && P == 0;
+  auto passes = [&]() {
+    if constexpr (EARLY) trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
+    {
+      double tr[N];
+      pass_P_any<N, P, FIRST || kLean>(p, acc, uv, lsP, tr, ci.sg[P], p.var[P]);
+      const unsigned char oP = ci.out[P];
+      if (oP == kOutCarry) store_vec<N>(gb.carry_out + N * r, tr, false);
+      else if (oP == kOutPub) store_vec<N>(p.tbuf[P] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
+    }
+    if constexpr (QA) {
+      double tr[N];
+      pass_Q_any<N, Q>(p, acc, uv, lsQ, tr, ci.sg[Q], p.var[Q]);
+      if (ci.out[Q] == kOutPub) store_vec<N>(p.tbuf[Q] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
+    }
+  };
+  // lean RK keeps reading the U buffer in its epilogue (U' = U + B_s dU): its fill comes at the very end
+  constexpr bool LATE_FILL = kLean && (MODE == kModeRK || MODE == kModeRKFirst);
+  if constexpr (kLean) {
+    // lean, last phase: every thread's reads of the U buffer are done after its passes -> barrier + the
+    // next group's fill (refill), reached by every thread
+    if (active) passes();
+    if constexpr (LAST && !LATE_FILL) refill(sR, R);
+  } else {
+    if constexpr (LAST) refill(sR, R);  // RK: dU into this thread's own accumulator slots (read above)
+    if (!active) return;
+    passes();
   }
-  HD_SUB(1);
-  if constexpr (QA) {
-    double tr[N];
-    pass_Q_any<N, Q>(p, acc, uv, lsQ, tr, ci.sg[Q], p.var[Q]);
-    if (ci.out[Q] == kOutPub) store_vec<N>(p.tbuf[Q] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
-  }
+  if (active) {
+  const size_t g0 = (size_t)ci.cell * G::ND + R;
   HD_SUB(2);
   // upwind traces (the staged ones have arrived once this thread's copies of this phase are complete)
-  cp_async_wait<WAIT>();
-  trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
+  if constexpr (!kLean) cp_async_wait<WAIT>();
+  if constexpr (!EARLY) trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
   if (ci.sg[P]) lift_P<N, 1>(acc, tP);
   else lift_P<N, 0>(acc, tP);
   HD_SUB(3);
@@ -609,6 +643,12 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
     trace_in<D, N, Q, SQ, SP>(p, ci, r, sR, R, gb, lsQ, stg_slot<N>(stg, PH, 1, tid), tQ);
     if (ci.sg[Q]) lift_Q<N, 1>(acc, tQ);
     else lift_Q<N, 0>(acc, tQ);
+  }
+  if constexpr (kLean && !FIRST) {
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int b = 0; b < N; ++b) acc[a][b] += gb.A[sidx<D, N>(sR, a * SP + b * SQ)];
   }
   HD_SUB(4);
 
@@ -638,7 +678,13 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   } else {
     // LSRK 2N stage: dU <- A_s dU + dt M^-1 A(U); U_new <- U + B_s dU. U is still in uv; dU arrived
     // (cp.async issued by stage_du) in this thread's own slots of the accumulator buffer.
-    if constexpr (MODE == kModeRK) {
+    if constexpr (MODE == kModeRK && kLean) {
+      // lean: dU straight from L2 (prefetched at the group start)
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) acc[a][b] = fma(p.rk_a, __ldcs(p.du + g0 + a * SP + b * SQ), acc[a][b]);
+    } else if constexpr (MODE == kModeRK) {
       cp_async_wait<0>();
 #pragma unroll
       for (int a = 0; a < N; ++a)
@@ -650,28 +696,36 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         __stcs(p.du + g0 + a * SP + b * SQ, acc[a][b]);
-        __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], uv[a][b]));
+        // lean: U re-read from the U buffer instead of keeping the tile live
+        const double u0 = kLean ? gb.U[sidx<D, N>(sR, a * SP + b * SQ)] : uv[a][b];
+        __stcs(p.out + g0 + a * SP + b * SQ, fma(p.rk_b, acc[a][b], u0));
       }
   }
   HD_SUB(5);
+  }  // active
+  if constexpr (LAST && LATE_FILL) refill(sR, R);  // every thread, after its U-buffer reads
 }
 
 // Shared-memory carve-up (offsets in doubles, every region 16-byte aligned):
 // bufs[3][CT*NDP] (two cell buffers alternating, one accumulator) | carry[2][CT*FN] | ptab[NPH][1024] |
-// stg[NPH][2][256][N] | info[2][CT] | raw[4][CT*D] | rawc[4][CT] (the schedule-record ring)
+// stg[NPH][2][256][N] | info[2][CT] | raw[4][CT*D] | rawc[4][CT] (the schedule-record ring) | uq[8] (unit
+// queue). Lean kernel: bufs[2] (U, accumulator), carry[1], no stg.
 __host__ __device__ constexpr int round2(int x) { return (x + 1) & ~1; }
 template <int D, int N>
 struct SmemMap {
-  int carry, ptab, stg, info, raw, rawc, bytes;
-  __host__ __device__ constexpr SmemMap(int CT) : carry(0), ptab(0), stg(0), info(0), raw(0), rawc(0), bytes(0) {
+  int carry, ptab, stg, info, raw, rawc, uq, bytes;
+  __host__ __device__ constexpr SmemMap(int CT)
+      : carry(0), ptab(0), stg(0), info(0), raw(0), rawc(0), uq(0), bytes(0) {
     using G = CGeo<D, N>;
-    carry = round2(3 * CT * G::NDP);
-    ptab = carry + round2(2 * CT * G::FN);
+    constexpr bool kLean = lean<D, N>();
+    carry = round2((kLean ? 2 : 3) * CT * G::NDP);
+    ptab = carry + round2((kLean ? 1 : 2) * CT * G::FN);
     stg = ptab + G::NPH * 1024;
-    info = stg + round2(G::NPH * 2 * 256 * N);
+    info = stg + (kLean ? 0 : round2(G::NPH * 2 * 256 * N));
     raw = info + round2(2 * CT * (int)sizeof(CellInfo) / 8);
     rawc = raw + 4 * CT * D * (int)sizeof(SchedDim) / 8;
-    bytes = (rawc + round2(4 * CT * (int)sizeof(SchedCell) / 8)) * 8;
+    uq = rawc + round2(4 * CT * (int)sizeof(SchedCell) / 8);
+    bytes = (uq + 4) * 8;
   }
 };
 static_assert(sizeof(CellInfo) % 8 == 0 && sizeof(SchedDim) % 16 == 0 && sizeof(SchedCell) == 8, "smem records");
@@ -695,8 +749,9 @@ __host__ __device__ constexpr int cell_smem_bytes() {
 // during the last phase. The progress flag of a group is released (st.release after a CTA barrier) at
 // the next group's start.
 template <int D, int N, int MODE>
-__global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constant__ CellParams p) {
+__global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const __grid_constant__ CellParams p) {
   using G = CGeo<D, N>;
+  constexpr bool kLean = lean<D, N>();
   constexpr int NPH = G::NPH;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int CT = p.CT;
@@ -771,15 +826,36 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     for (int q = tid; q < nitems * 2; q += nthr) cp_async16(dst + 16 * q, src + 16 * q);
     for (int q = tid; q < CT; q += nthr) cp_async8(rawc + slot * MAXCT + q, p.schedc + gs * CT + q);
   };
-  // the CTA's group sequence: iteration it -> (unit, step); j groups ahead of (u0, g0)
+  // the CTA's group sequence: iteration it -> (unit, step); j groups ahead of (u0, g0). Dynamic dealing
+  // (HD_DYN): after its first unit (u_begin + blockIdx) a CTA takes the next unit from the launch's counter;
+  // the units it will run are queued in smem (uq[k & 7] = its k-th unit, qk = the current one), grabbed by
+  // one thread a group before anybody reads them. Units still start in increasing order, so the published-
+  // trace protocol is unchanged, and a CTA that runs slower than its SM neighbour takes fewer units.
+  int *uq = reinterpret_cast<int *>(smem + map.uq);
+  int qk = 0, ngrab = 1;
   auto ahead = [&](int u0, int g0, int j, int &uo, int &go) {
     uo = u0;
     go = g0 + j;
-    while (go >= p.GPU) {
-      go -= p.GPU;
-      uo += gridDim.x;
+    if constexpr (kDyn) {
+      int k = qk;
+      while (go >= p.GPU) {
+        go -= p.GPU;
+        ++k;
+      }
+      if (k != qk) uo = uq[k & 7];
+    } else {
+      while (go >= p.GPU) {
+        go -= p.GPU;
+        uo += gridDim.x;
+      }
     }
     return uo < p.u_end;
+  };
+  auto grab_upto = [&](int kneed) {  // one thread: queue the units up to the kneed-th
+    while (ngrab <= kneed) {
+      uq[ngrab & 7] = p.u_begin + (int)gridDim.x + atomicAdd(p.uctr, 1);
+      ++ngrab;
+    }
   };
   const int nwarps = nthr >> 5;
   const int item0 = nitems <= nthr ? (tid & 31) * nwarps + (tid >> 5) : tid;
@@ -809,7 +885,11 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       unsigned char src = rr.src;
       const double *ts = nullptr;
       if (src == kSrcPub) {
-        if ((j == 0 ? fv0 : fv1) >= (p.epoch | rr.need)) {
+        // flags read in phase 1 (acquire); a producer that was not done then gets a second look now, two
+        // phases later -- a producer running only slightly behind its nominal lead is then usually done
+        int fv = j == 0 ? fv0 : fv1;
+        if (fv < (p.epoch | rr.need)) fv = ld_acquire(p.flags + rr.pflag);
+        if (fv >= (p.epoch | rr.need)) {
           ts = p.tbuf[i] + (size_t)rr.slot * p.FN;
         } else {
           src = kSrcDirect;  // not published yet: read the neighbour cell itself
@@ -819,6 +899,10 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
         ts = p.hbuf[i] + (size_t)rr.slot * p.FN;
       }
       if (src == kSrcDirect) ts = p.u + (size_t)rr.nb * p.ND;
+#ifdef HD_COUNT
+      if (rr.src == kSrcPub) atomicAdd(p.err + (src == kSrcPub ? 25 : 26), 1);
+      else if (src == kSrcDirect) atomicAdd(p.err + 27, 1);
+#endif
       HD_DCHECK(p, rc[kc].cell >= 0 && rc[kc].cell < p.ncells && rr.nb >= 0 && rr.nb < p.ncells, 1);
       HD_DCHECK(p, src != kSrcPub || (rr.slot >= 0 && rr.slot < p.ncells && rr.pflag >= 0 && rr.pflag < p.nunits), 1);
       HD_DCHECK(p, src != kSrcGroup || (rr.slot >= 0 && rr.slot < CT), 1);
@@ -838,6 +922,13 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
   };
 
   int u = p.u_begin + (int)blockIdx.x, gi = 0, it = 0;
+  if constexpr (kDyn) {
+    if (tid == nthr - 1) {
+      uq[0] = u;
+      grab_upto(4 / p.GPU);
+    }
+    __syncthreads();
+  }
   // prologue: the records of the first three groups, group 0's schedule and cells
   for (int j = 0; j < kRing - 1; ++j) {
     int ua, ga;
@@ -862,16 +953,19 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     HD_PROF_BAR(0);
     HD_PROF_GROUP();
     if (prev_unit >= 0 && tid == nthr - 1) st_release(p.flags + prev_unit, p.epoch | (prev_step + 1));
+    // the units the next group's lookahead reaches (read after the next barrier)
+    if (kDyn && tid == nthr - 1) grab_upto(qk + (gi + 4) / p.GPU);
     const CellInfo &ci = info0[s * MAXCT + kk0];
     GroupBufs gb;
-    gb.Ugrp = bufs + s * CND;
+    gb.Ugrp = bufs + (kLean ? 0 : s) * CND;
     gb.U = gb.Ugrp + (size_t)kk0 * G::NDP;
-    gb.A = bufs + 2 * CND + (size_t)kk0 * G::NDP;
-    gb.carry = carry0 + (size_t)(s * MAXCT + kk0) * G::FN;
-    gb.carry_out = carry0 + (size_t)((s ^ 1) * MAXCT + kk0) * G::FN;
+    gb.A = bufs + (kLean ? 1 : 2) * CND + (size_t)kk0 * G::NDP;
+    gb.carry = carry0 + (size_t)((kLean ? 0 : s) * MAXCT + kk0) * G::FN;
+    gb.carry_out = carry0 + (size_t)((kLean ? 0 : s ^ 1) * MAXCT + kk0) * G::FN;
     // cp.async groups of this thread, in commit order: this group's staged traces per phase, the records of
     // the group three ahead, then (last phase) RK dU and the next group's cells
-    if (active) {
+    if constexpr (kLean) {
+    } else if (active) {
       stage_phase<D, N, 0>(ci, r, stg, tid);
       if constexpr (NPH > 1) stage_phase<D, N, (NPH > 1 ? 1 : 0)>(ci, r, stg, tid);
       if constexpr (NPH > 2) stage_phase<D, N, (NPH > 2 ? 2 : 0)>(ci, r, stg, tid);
@@ -884,29 +978,38 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
       if (ahead(u, gi, kRing - 1, ua, ga)) fetch((it + kRing - 1) % kRing, (long long)ua * p.GPU + ga);
       cp_async_commit();
     }
-    if (MODE == kModeRK && tid == 0 && p.prefetch)
+    if (!kLean && MODE == kModeRK && tid == 0 && p.prefetch)
       for (int kc = 0; kc < CT; ++kc)
         prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
     HD_MARK(1);
     auto flags_next = [&]() {
       if (has_next) {
         acquire(slot1);
-        // the cells of the group after next into L2 (its fill is issued at the next group's start)
+        // the cells of the group after next into L2 (its fill is issued at the next group's start); lean: the
+        // next group's (its fill is issued in this group's last phase) -- with two CTAs per SM a group takes
+        // twice as long, and two groups of HBM traffic would cycle the whole L2 before the fill
         int ua, ga;
-        if (tid == 0 && p.prefetch && ahead(u, gi, 2, ua, ga)) {
-          const int slot2 = (it + 2) % kRing;
+        constexpr int kAhead = kLean ? HD_LEAN_PF : 2;
+        if (tid == 0 && p.prefetch && kAhead > 0 && ahead(u, gi, kAhead, ua, ga)) {
+          const int slot2 = (it + kAhead) % kRing;
           for (int kc = 0; kc < CT; ++kc)
             prefetch_l2(p.u + ((size_t)rawc[slot2 * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
         }
       }
+      // lean RK: this group's dU into L2 for the epilogue's direct reads
+      if (kLean && MODE == kModeRK && tid == 32 && p.prefetch)
+        for (int kc = 0; kc < CT; ++kc)
+          prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
     };
     // the next group's cells stream into the other cell buffer (free since the previous group ended)
-    if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs + (s ^ 1) * CND);
-    cp_async_commit();
+    if constexpr (!kLean) {
+      if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs + (s ^ 1) * CND);
+      cp_async_commit();
+    }
     HD_MARK(2);
     auto refill = [&](int sR, int R) {
       // RK: dU of this thread's tile into its own (already read) accumulator slots
-      if constexpr (MODE == kModeRK) {
+      if constexpr (MODE == kModeRK && !kLean) {
         if (active) {
           constexpr int P = G::P(NPH - 1), Q = G::Q(NPH - 1);
           constexpr int SP = ipow(N, P), SQ = ipow(N, Q);
@@ -916,6 +1019,12 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
 #pragma unroll
             for (int b = 0; b < N; ++b) cp_async8(gb.A + sidx<D, N>(sR, a * SP + b * SQ), src + a * SP + b * SQ);
         }
+        cp_async_commit();
+      }
+      if constexpr (kLean) {
+        // every thread has read its last-phase tiles: the next group's cells stream into the U buffer
+        __syncthreads();
+        if (has_next) copy_cells(rawc[slot1 * MAXCT].cell, bufs);
         cp_async_commit();
       }
     };
@@ -947,6 +1056,7 @@ __global__ void __launch_bounds__(256, HD_MINB) cell_kernel(const __grid_constan
     cp_async_wait<0>();  // the next group's cells (and the records fetched this group)
     prev_unit = p.flags ? u : -1;
     prev_step = gi;
+    if (gi + 1 >= p.GPU) ++qk;
     u = un;
     gi = gn;
     ++it;

@@ -103,6 +103,7 @@ struct CellParams {
   const SchedDim *sched;  // [nunits * GPU][CT][D]
   const SchedCell *schedc;  // [nunits * GPU][CT]
   int *flags;             // [nunits rounded up to 4] unit progress flags
+  int *uctr;              // unit counter of the launch (dynamic unit dealing; zeroed before every launch)
   double *tbuf[kMaxD];    // published traces per dim: [slot][n^(d-1)]
   const double *hbuf[kMaxD];  // received halo traces per x dim: [slot][n^(d-1)]
   int var[kMaxD];         // 1: a_i depends on z (line speeds vary: u is scaled per line); 0: constant
