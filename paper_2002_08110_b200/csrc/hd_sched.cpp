@@ -20,6 +20,7 @@
 // rank-1 folding of DESIGN.md §6): the dim-0 carry of the previous step (smem), an in-group neighbour
 // (smem), a trace published by an earlier unit (checked against its progress flag at run time, else a
 // direct read), the halo receive buffer (multi-rank), or a direct read of the neighbour cell.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -35,6 +36,9 @@ struct Geo {
   int follow[kMaxD], pub[kMaxD], xsplit[kMaxD];
   long long UC;
   const hd_mesh *m;
+  // wavefront unit order (pencil mode, one v-chunk): order[u] = the lexicographic index of unit u, rank =
+  // its inverse; empty = lexicographic
+  std::vector<long long> order, rank;
 };
 
 // a_i at the lower corner of the cell with local coordinates c and its sign on the cell (evaluated at the
@@ -62,6 +66,7 @@ struct Unit {
 // traversal coordinates of pencil-mode unit u -> the unit's first cell coordinates, dim-0 direction, start
 long long pencil_decode(const Geo &g, long long u, long long *c, int &dir0, int &skew) {
   long long base = 0, tsum = 0;
+  if (!g.order.empty()) u = g.order[(size_t)u];
   for (int j = 0; j < kMaxD; ++j) c[j] = 0;
   for (int j = g.d - 1; j >= 1; --j) {
     const long long ext = j == 1 ? g.L[1] / g.CT : g.L[j];
@@ -95,7 +100,7 @@ long long unit_of(const Geo &g, const long long *c) {
     const long long cj = j == 1 ? c[1] / g.CT : c[j];
     u += (neg ? ext - 1 - cj : cj) * g.ustride[j];
   }
-  return u;
+  return g.rank.empty() ? u : g.rank[(size_t)u];
 }
 
 int step_group(const Geo &g, int gi, int dir0, int skew) {
@@ -165,6 +170,35 @@ void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<Sc
     g.xsplit[i] = m.pt.parts[i] > 1 ? 1 : 0;
   }
   g.UC = g.pencil ? g.L[0] * g.CT : g.CT;
+  if (g.pencil && m.nchunk == 1 && m.nunits > 1) {
+    // Wavefront order: units sorted by the sum of their traversal coordinates (stable). Every upwind
+    // neighbour of a unit lies on the previous hyperplane, so it still comes earlier, but units dealt
+    // together (one round of CTAs) are rarely neighbours: the producer of a published trace has usually
+    // finished its whole pencil, and the skew seams (a same-round consumer's first `skew` steps, whose
+    // producer processes those cells last) become rare.
+    const long long nu = m.nunits;
+    std::vector<int> key((size_t)nu);
+    int kmax = 0;
+    for (long long u = 0; u < nu; ++u) {
+      int t = 0;
+      for (int j = 1; j < g.d; ++j) {
+        const long long ext = (j == 1 && g.pencil) ? g.L[1] / g.CT : g.L[j];
+        t += (int)((u / g.ustride[j]) % ext);
+      }
+      key[(size_t)u] = t;
+      kmax = std::max(kmax, t);
+    }
+    std::vector<long long> start((size_t)kmax + 2, 0);
+    for (long long u = 0; u < nu; ++u) ++start[(size_t)key[(size_t)u] + 1];
+    for (int k = 0; k <= kmax; ++k) start[(size_t)k + 1] += start[(size_t)k];
+    g.order.assign((size_t)nu, 0);
+    g.rank.assign((size_t)nu, 0);
+    for (long long u = 0; u < nu; ++u) {
+      const long long pos = start[(size_t)key[(size_t)u]]++;
+      g.order[(size_t)pos] = u;
+      g.rank[(size_t)u] = pos;
+    }
+  }
   const int d = g.d, CT = g.CT, GPU = g.GPU;
   out.assign((size_t)m.nunits * GPU * CT * d, SchedDim{});
   cells.assign((size_t)m.nunits * GPU * CT, SchedCell{});
