@@ -32,6 +32,15 @@
 #ifndef HD_PF_PUB
 #define HD_PF_PUB 1
 #endif
+#ifndef HD_PF_DIRECT
+#define HD_PF_DIRECT 2
+#endif
+#ifndef HD_PF_DU
+#define HD_PF_DU 2
+#endif
+#ifndef HD_FILL_EF
+#define HD_FILL_EF 1
+#endif
 #ifndef HD_DYN
 #define HD_DYN 1
 #endif
@@ -784,6 +793,7 @@ __global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const _
   constexpr bool FASTFILL = N == 4 && G::NT * MAXCT == 256 && (G::ND % 512 == 0 || 512 % G::ND == 0);
   const int fbase = swz<D, N>((2 * tid) % G::ND);
   const int fcell0 = (2 * tid) / G::ND;
+  const unsigned long long pol_ef = HD_FILL_EF ? l2_policy_evict_first() : 0ull;
   auto copy_cells = [&](int first_cell, double *dst) {
     HD_DCHECK(p, first_cell >= 0 && first_cell + (CT - 1) * p.cstride < p.ncells, 1);
     if constexpr (FASTFILL) {
@@ -793,7 +803,10 @@ __global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const _
             const double *src = p.u + ((size_t)first_cell + kc * p.cstride) * G::ND + 2 * tid;
             double *d0 = dst + kc * G::NDP + fbase;
 #pragma unroll
-            for (int m = 0; m < G::ND / 512; ++m) cp_async16(d0 + swz<D, N>(512 * m), src + 512 * m);
+            for (int m = 0; m < G::ND / 512; ++m) {
+              if constexpr (HD_FILL_EF) cp_async16_hint(d0 + swz<D, N>(512 * m), src + 512 * m, pol_ef);
+              else cp_async16(d0 + swz<D, N>(512 * m), src + 512 * m);
+            }
           }
         } else {
           for (int j = 0; j < CT * G::ND / 512; ++j) {
@@ -870,7 +883,7 @@ __global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const _
         const int v = ld_acquire(p.flags + rr.pflag);
         if (j == 0) fv0 = v;
         else fv1 = v;
-      } else if (rr.src == kSrcDirect && p.prefetch) {
+      } else if (rr.src == kSrcDirect && p.prefetch && HD_PF_DIRECT == 1) {
         prefetch_l2(p.u + (size_t)rr.nb * p.ND, (unsigned)(p.ND * 8));
       }
     }
@@ -903,6 +916,7 @@ __global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const _
         if (HD_PF_PUB && p.prefetch) prefetch_l2(ts, (unsigned)(p.FN * 8));
       }
       if (src == kSrcDirect) ts = p.u + (size_t)rr.nb * p.ND;
+      if (HD_PF_DIRECT == 2 && rr.src == kSrcDirect && p.prefetch) prefetch_l2(ts, (unsigned)(p.ND * 8));
 #ifdef HD_COUNT
       if (rr.src == kSrcPub) atomicAdd(p.err + (src == kSrcPub ? 25 : 26), 1);
       else if (src == kSrcDirect) atomicAdd(p.err + 27, 1);
@@ -1001,7 +1015,7 @@ __global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const _
         }
       }
       // lean RK: this group's dU into L2 for the epilogue's direct reads
-      if (kLean && MODE == kModeRK && tid == 32 && p.prefetch)
+      if (kLean && MODE == kModeRK && tid == 32 && p.prefetch && HD_PF_DU == 1)
         for (int kc = 0; kc < CT; ++kc)
           prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
     };
@@ -1051,6 +1065,9 @@ __global__ void __launch_bounds__(256, lean<D, N>() ? 2 : 1) cell_kernel(const _
         run_phase<D, N, MODE, (NPH > 1 ? 1 : 0), 3>(p, ci, ptab, stg, r, gb, active, none, HD_PF(1));
         HD_MARK(5);
         HD_PROF_BAR(2);
+        if (kLean && MODE == kModeRK && tid == 32 && p.prefetch && HD_PF_DU == 2)
+          for (int kc = 0; kc < CT; ++kc)
+            prefetch_l2(p.du + ((size_t)info0[s * MAXCT].cell + kc * p.cstride) * G::ND, (unsigned)(G::ND * 8));
         run_phase<D, N, MODE, (NPH > 2 ? 2 : 0), WLAST>(p, ci, ptab, stg, r, gb, active, refill, HD_PF(2));
         HD_MARK(6);
       }
