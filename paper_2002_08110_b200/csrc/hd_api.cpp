@@ -115,11 +115,12 @@ void fill_cell_params(hd_mesh *m, hd::CellParams &p) {
   const int d = m->d, n = m->n;
   const hd::CellGeometry &g = m->geo;
   p.CT = g.CT;
-  p.GPU = g.GPU;
+  p.GPU = g.GPU * m->slab;
+  p.slab = m->slab;
   p.FN = (int)(m->nd / m->n);
   p.ND = (int)m->nd;
   p.prefetch = (m->nd * 8) % 16 == 0 ? 1 : 0;
-  p.nunits = m->nunits;
+  p.nunits = m->nunits / m->slab;
   p.jdet = m->jdet;
   p.cstride = g.pencil ? m->pt.len[0] : 1;
   p.sched = m->sched;
@@ -271,6 +272,9 @@ hd_status plan_traces(hd_mesh *m) {
   m->epoch = 0;
   // skew (steps a same-round producer runs ahead of its consumer): 2 gives the producer a full step of
   // margin; the first `skew` steps of a pencil then read their upwind neighbours directly
+#ifndef HD_SLAB
+#define HD_SLAB 0
+#endif
 #ifndef HD_SKEW
 #define HD_SKEW 2
 #endif
@@ -622,6 +626,7 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
     m->geo = hd::cell_geometry(d, n, (int)pt.len[0], (int)pt.len[1], m->ncells_local, pencil_ok);
   }
   m->nunits = (int)(m->geo.pencil ? m->ncells_local / (pt.len[0] * m->geo.CT) : m->ncells_local / m->geo.CT);
+  m->slab = 1;
   e = hd::cell_grid_size(d, n, m->geo, m->sms, &m->grid);
   if (e != cudaSuccess) {
     delete m;
@@ -646,7 +651,16 @@ hd_status hd_create_mesh(const hd_mesh_desc *desc, hd_mesh **out) {
       e2 = cudaEventCreateWithFlags(&m->ev_chunk[c], cudaEventDisableTiming);
     if (e2 != cudaSuccess) st = cuda_fail(e2, "halo stream / events");
   }
-  if (st == HD_OK) st = upload_schedule(m);
+  if (st == HD_OK) {
+    // slab super-units (one-chunk pencil meshes whose dim 1 publishes and is traversed upwind first): the
+    // dim-1 traces then stay inside one CTA, one row of the slab apart -- kept in L2.
+    // Off by default (HD_SLAB=1 builds it): 6% less DRAM traffic per 6D stage, but 1.4% slower (6D) and 5%
+    // slower (5D: small wavefront hyperplanes of slabs put producers in their consumers' round)
+    const int R = m->geo.pencil ? (int)(m->pt.len[1] / m->geo.CT) : 1;
+    m->slab = (HD_SLAB && m->nchunk == 1 && R > 1 && m->pub[1] && m->follow[1] && (long long)R * m->geo.GPU < 1000) ? R : 1;
+    if (m->nchunk == 1) m->chunk_u[1] = m->nunits / m->slab;
+    st = upload_schedule(m);
+  }
   if (st == HD_OK && desc->nranks > 1 && desc->nccl_id) {
     st = load_nccl();
     if (st == HD_OK) {
@@ -947,20 +961,20 @@ hd_status launch_stage(hd_mesh *m, hd::CellParams &p, const double *U, double *d
     if (st != HD_OK) return st;
     p.sched = m->sched;
     p.schedc = m->schedc;
-    st = launch_units(m, p, 0, m->nunits, s);
+    st = launch_units(m, p, 0, m->nunits / m->slab, s);
     if (st == HD_OK) st = begin_stage(m, p, U, dU, out, mode == hd::kModeAdvection ? hd::kModeAdvAcc : hd::kModeRK,
                                       mode == hd::kModeAdvection ? 0.0 : 1.0, b, s);
     if (st != HD_OK) return st;
     p.sched = m->sched2;
     p.schedc = m->schedc2;
-    st = launch_units(m, p, 0, m->nunits, s);
+    st = launch_units(m, p, 0, m->nunits / m->slab, s);
     p.sched = m->sched;
     p.schedc = m->schedc;
     return st;
   }
   hd_status st = begin_stage(m, p, U, dU, out, mode, a, b, s);
   if (st != HD_OK) return st;
-  if (m->desc.nranks == 1) return launch_units(m, p, 0, m->nunits, s);
+  if (m->desc.nranks == 1) return launch_units(m, p, 0, m->nunits / m->slab, s);
   cudaError_t e = cudaEventRecord(m->ev_u, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(m->comm, m->ev_u, 0);
   if (e != cudaSuccess) return cuda_fail(e, "halo stream order");

@@ -237,6 +237,10 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// Drop a 128-byte L2 line without writing it back (its data becomes undefined).
+__device__ __forceinline__ void discard_l2(const void *p) {
+  asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
+}
 // Bring a whole cell (contiguous, 16-byte multiple) into L2 ahead of its read.
 __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
@@ -386,6 +390,16 @@ __device__ __forceinline__ void store_vec(double *dst, const double (&t)[N], boo
       else dst[j] = t[j];
     }
   }
+}
+// N (even) values with the L2 evict_last policy: data this CTA reads back soon, to survive the streams
+template <int N>
+__device__ __forceinline__ void store_vec_keep(double *dst, const double (&t)[N]) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+#pragma unroll
+  for (int j = 0; j < N; j += 2)
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(dst + j), "d"(t[j]), "d"(t[j + 1]), "l"(pol)
+                 : "memory");
 }
 template <int N>
 __device__ __forceinline__ void load_vec(const double *src, double (&t)[N], bool global) {
@@ -622,7 +636,17 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
       pass_P_any<N, P, FIRST || kLean>(p, acc, uv, lsP, tr, ci.sg[P], p.var[P]);
       const unsigned char oP = ci.out[P];
       if (oP == kOutCarry) store_vec<N>(gb.carry_out + N * r, tr, false);
-      else if (oP == kOutPub) store_vec<N>(p.tbuf[P] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
+      else if (oP == kOutPub) {
+        // slab super-units: the dim-1 trace is read by this CTA one slab row later -- keep it in L2
+        bool kept = false;
+        if constexpr (P == 1 && kLean && N % 2 == 0) {
+          if (p.slab > 1) {
+            store_vec_keep<N>(p.tbuf[P] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr);
+            kept = true;
+          }
+        }
+        if (!kept) store_vec<N>(p.tbuf[P] + (size_t)ci.oslot * G::FN + (size_t)N * r, tr, true);
+      }
     }
     if constexpr (QA) {
       double tr[N];
@@ -648,6 +672,14 @@ __device__ __forceinline__ void run_phase(const CellParams &p, const CellInfo &c
   if constexpr (!EARLY) trace_in<D, N, P, SP, SQ>(p, ci, r, sR, R, gb, lsP, stg_slot<N>(stg, PH, 0, tid), tP);
   if (ci.sg[P]) lift_P<N, 1>(acc, tP);
   else lift_P<N, 0>(acc, tP);
+  if constexpr (kLean && P == 1 && N == 4 && D >= 5) {
+    // slab super-units: a consumed dim-1 trace has no other reader -- once the warp's lifts used every lane's
+    // values, drop its lines from L2 without a write-back (one lane per 128-byte line of 4 threads' traces)
+    if (p.slab > 1 && ci.src[1] == kSrcPub) {
+      __syncwarp();
+      if ((tid & 3) == 0) discard_l2(ci.tsrc[1] + N * r);
+    }
+  }
   HD_SUB(3);
   if constexpr (QA) {
     trace_in<D, N, Q, SQ, SP>(p, ci, r, sR, R, gb, lsQ, stg_slot<N>(stg, PH, 1, tid), tQ);

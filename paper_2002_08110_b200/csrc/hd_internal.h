@@ -104,6 +104,8 @@ struct CellParams {
   const SchedCell *schedc;  // [nunits * GPU][CT]
   int *flags;             // [nunits rounded up to 4] unit progress flags
   int *uctr;              // unit counter of the launch (dynamic unit dealing; zeroed before every launch)
+  int slab;               // > 1: slab super-units -- dim-1 published traces are this CTA's own (L2 evict_last,
+                          // discarded once read)
   double *tbuf[kMaxD];    // published traces per dim: [slot][n^(d-1)]
   const double *hbuf[kMaxD];  // received halo traces per x dim: [slot][n^(d-1)]
   int var[kMaxD];         // 1: a_i depends on z (line speeds vary: u is scaled per line); 0: constant
@@ -202,6 +204,9 @@ struct hd_mesh {
   // trace machinery (device buffers owned by the mesh)
   hd::CellGeometry geo;
   int nunits;
+  // slab super-units: the kernel runs `slab` consecutive pencil units (the pencils of one
+  // dim-0/dim-1 slab, dim-1 traversal order) as one unit of slab * GPU steps; 1 = pencil units
+  int slab;
   int pub[6], follow[6];
   int skew;                // pencil mode: a unit starts at step (-skew * sum_j t_j) mod GPU (hd_sched.cpp)
   double *tbuf[6];

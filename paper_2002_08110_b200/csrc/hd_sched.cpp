@@ -30,7 +30,7 @@ namespace hd {
 namespace {
 
 struct Geo {
-  int d, CT, GPU, pencil, skew;
+  int d, CT, GPU, pencil, skew, slab;
   int forced;  // -1: the sign of a_i decides the upwind side; 0 / 1: every dim takes its left / right neighbour
   long long L[kMaxD], lstride[kMaxD], ustride[kMaxD], off[kMaxD];
   int follow[kMaxD], pub[kMaxD], xsplit[kMaxD];
@@ -155,6 +155,7 @@ void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<Sc
   g.GPU = m.geo.GPU;
   g.pencil = m.geo.pencil;
   g.skew = m.skew;
+  g.slab = m.slab;
   long long ls = 1, us = 1;
   for (int i = 0; i < g.d; ++i) {
     g.L[i] = m.pt.len[i];
@@ -175,13 +176,15 @@ void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<Sc
     // neighbour of a unit lies on the previous hyperplane, so it still comes earlier, but units dealt
     // together (one round of CTAs) are rarely neighbours: the producer of a published trace has usually
     // finished its whole pencil, and the skew seams (a same-round consumer's first `skew` steps, whose
-    // producer processes those cells last) become rare.
+    // producer processes those cells last) become rare. Slab super-units (slab > 1): the key leaves out
+    // t_1, so the slab's pencils (t_1 = 0 .. slab-1, lexicographic index fastest in t_1) stay consecutive
+    // -- kernel unit U = pencil units U*slab .. U*slab + slab-1, run one after the other.
     const long long nu = m.nunits;
     std::vector<int> key((size_t)nu);
     int kmax = 0;
     for (long long u = 0; u < nu; ++u) {
       int t = 0;
-      for (int j = 1; j < g.d; ++j) {
+      for (int j = g.slab > 1 ? 2 : 1; j < g.d; ++j) {
         const long long ext = (j == 1 && g.pencil) ? g.L[1] / g.CT : g.L[j];
         t += (int)((u / g.ustride[j]) % ext);
       }
@@ -271,8 +274,9 @@ void build_schedule(const hd_mesh &m, std::vector<SchedDim> &out, std::vector<Sc
             // neighbour's group is done", and the neighbour's slot in the producer unit (same pencil and
             // c_0, except along dim 1 where it is the other end of the neighbouring block)
             src = kSrcPub;
-            pflag = (int)ui.pu[i];
-            need = group_step(g, (int)c[0], ui.pdir0[i], ui.pskew[i]) + 1;
+            // flags and steps are per kernel unit: a slab super-unit runs its pencils one after the other
+            pflag = (int)(ui.pu[i] / g.slab);
+            need = (int)(ui.pu[i] % g.slab) * GPU + group_step(g, (int)c[0], ui.pdir0[i], ui.pskew[i]) + 1;
             const long long kn = (g.pencil && i == 1) ? (k + up + CT) % CT : k;
             slot = ui.pu[i] * g.UC + (g.pencil ? kn * g.L[0] + c[0] : kn);
           }
