@@ -141,9 +141,10 @@ hd_status hd_fill_initial(hd_mesh *m, double *u, int recipe, unsigned long long 
 hd_status hd_tables_1d(int n, double *xi, double *w, double *K, double *lam, double *tau);
 hd_status hd_lsrk_coefficients(double *a, double *b);
 
-/* Upwind-trace plan of the mesh per dimension: tmode[i] = 0 (the cell
- * reads its upwind neighbour itself or gets it from the same CTA), 1 (published into a ring of
- * ring_slots[i] trace slots), 2 (published into a full-size buffer, one slot per cell). */
+/* Upwind-trace plan of the mesh per dimension (DESIGN.md §6 "Upwind trace sources"): tmode[i] = 0 (the
+ * cell reads its upwind neighbour itself or gets it from the same CTA) or 2 (published into a full-size
+ * buffer, one n^(d-1)-value slot per cell). Mode 1 (an L2-sized ring of slots) is reserved and not built:
+ * ring_slots[i] is always 0. */
 hd_status hd_mesh_traces(const hd_mesh *m, int *tmode, int *ring_slots);
 
 /* 128-byte ncclUniqueId for hd_mesh_desc.nccl_id (rank 0 creates it and broadcasts it). Loads
