@@ -1,6 +1,6 @@
 #!/bin/bash
 # Experiment builds (bench configs only): tools/build_variant.sh <git-ref|cur> <out.so> [extra -D flags]
-# cur = the working tree. The library lands in paper_2002_08110_b200/<out.so> (A/B with tools/run_ab.sh).
+# cur = the working tree. The library lands in paper_2002_08110_b200/<out.so> (A/B with tools/gpu_ab_only.sh).
 ref=$1; out=$2; shift 2
 R=$(cd "$(dirname "$0")/.." && pwd)
 W=/tmp/bv_$out; rm -rf $W; mkdir -p $W/paper_2002_08110_b200/csrc $W/include
