@@ -342,6 +342,27 @@ def run_gpu(args):
                          "hbm_frac_of_measured_32B": value * 32 / peak / world,
                          "hbm_frac_of_measured_30.4B": value * 30.4 / peak / world},
         }
+        # the face-centric loop comparison path (hd_apply_advection_fcl) where its
+        # face buffers (3 d n^(d-1) doubles per cell) fit beside the product path's buffers
+        dd, nn = spec["d_x"] + spec["d_v"], spec["k"] + 1
+        fcl_bytes = 3 * dd * (N // nn) * 8
+        if world == 1 and not args.no_fcl:
+            free = torch.cuda.mem_get_info()[0]
+            if fcl_bytes < free - (1 << 30):
+                for _ in range(2):
+                    mesh.apply_advection_fcl(u, v, 0.0, stream)
+                barrier()
+                f_ms = timed(lambda: mesh.apply_advection_fcl(u, v, 0.0, stream), reps) / reps
+                f_gdofs = ndofs / (f_ms * 1e-3) / 1e9
+                design = 32.0 + 6 * dd * 8.0 / nn
+                extra["apply_advection_fcl"] = {
+                    "gdofs": f_gdofs, "ms": f_ms, "ecl_over_fcl": a_gdofs / f_gdofs,
+                    "roofline": dict(op_roofline(f_gdofs, "fcl_cell + fcl_face + fcl_lift (v <- A(u), face-centric loop)",
+                                                 "fcl"),
+                                     design_bytes_per_dof=design, frac_design=f_gdofs * design / (peak * world))}
+            else:
+                extra["apply_advection_fcl"] = {"skipped": f"face buffers ({fcl_bytes / 1e9:.1f} GB) do not fit the "
+                                                           f"{free / 1e9:.1f} GB left beside the product path's buffers"}
         # keep the solution buffer intact for e2e: u, v, w are distinct
         mesh.fill_initial(bufs[0], cfg["recipe"], seed)
         sol = 0
@@ -416,6 +437,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ops", action="store_true")
+    ap.add_argument("--no-fcl", action="store_true", help="skip the face-centric loop comparison timing")
     ap.add_argument("--l2-flush", action="store_true", help="flush L2 between timed repetitions (3D/4D)")
     ap.add_argument("--partition", default="auto", choices=["auto", "slabs"],
                     help="multi-GPU x partition: smallest halo (auto) or x-slabs of the slowest x dim")

@@ -98,6 +98,16 @@ hd_status hd_mesh_box(const hd_mesh *m, long long *off, long long *len, int *xpa
  * (HD_ERR_ARG otherwise). t is the evaluation time (the built fields do not depend on t). */
 hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream);
 
+/* v <- A(u) through the face-centric loop (FCL) the paper compares against its element-centric default
+ * (SURVEY §8(f) NEXT-3): a cell pass (volume term and both face traces of every dim),
+ * a face pass (each face's numerical flux computed once, upwind or central by desc.flux) and a
+ * lift pass (the flux tested on both sides). Same result as hd_apply_advection up to rounding order.
+ * u, v: non-overlapping device vectors of owned_dofs doubles (HD_ERR_ARG otherwise). The first call
+ * allocates the mesh's face buffers, 3 d n^(d-1) doubles per cell (HD_ERR_OOM if they do not fit; freed by
+ * hd_destroy_mesh). Single-rank meshes whose cell fits 200 KB of shared memory (HD_ERR_UNSUPPORTED
+ * otherwise). Three kernel launches on stream. */
+hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double t, void *stream);
+
 /* u <- M^-1 u and u <- M u, in place; one streaming pass, no communication. */
 hd_status hd_apply_inv_mass(hd_mesh *m, double *u, void *stream);
 hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream);

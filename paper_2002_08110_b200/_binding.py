@@ -33,7 +33,7 @@ class HdMeshDesc(ctypes.Structure):
 _lib = None
 
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection",
+EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection", "hd_apply_advection_fcl",
            "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_stage", "hd_rk_step_host", "hd_apply_advection_group",
            "hd_rk_step_group", "hd_fill_initial", "hd_tables_1d", "hd_lsrk_coefficients", "hd_mesh_traces",
            "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_halo_chunks", "hd_launch_count", "hd_last_error"]
@@ -53,6 +53,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_destroy_mesh.argtypes = [vp]
     lib.hd_mesh_info.argtypes = [vp, P(ll), P(ll), P(ll)]
     lib.hd_apply_advection.argtypes = [vp, vp, vp, ctypes.c_double, vp]
+    lib.hd_apply_advection_fcl.argtypes = [vp, vp, vp, ctypes.c_double, vp]
     lib.hd_apply_inv_mass.argtypes = [vp, vp, vp]
     lib.hd_apply_mass.argtypes = [vp, vp, vp]
     lib.hd_rk_step.argtypes = [vp, P(vp), P(ctypes.c_int), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
@@ -229,6 +230,12 @@ class Mesh:
     def apply_advection(self, u, v, t: float = 0.0, stream=None):
         _check(load_library().hd_apply_advection(self._h, self._vec(u, "u"), self._vec(v, "v"), float(t),
                                                  _stream_handle(stream)))
+        return v
+
+    def apply_advection_fcl(self, u, v, t: float = 0.0, stream=None):
+        """v <- A(u) through the face-centric loop comparison path (hd.h hd_apply_advection_fcl)."""
+        _check(load_library().hd_apply_advection_fcl(self._h, self._vec(u, "u"), self._vec(v, "v"), float(t),
+                                                     _stream_handle(stream)))
         return v
 
     def apply_inv_mass(self, u, stream=None):

@@ -207,6 +207,8 @@ void free_mesh(hd_mesh *m) {
   if (m->pack_cells) cudaFree(m->pack_cells);
   if (m->pack_dimsg) cudaFree(m->pack_dimsg);
   if (m->sendbuf) cudaFree(m->sendbuf);
+  if (m->fcl_tr) cudaFree(m->fcl_tr);
+  if (m->fcl_G) cudaFree(m->fcl_G);
   if (m->nccl_comm && g_nccl.ok) g_nccl.comm_destroy(m->nccl_comm);
   for (int c = 0; c < hd::kMaxChunk; ++c)
     if (m->ev_chunk[c]) cudaEventDestroy(m->ev_chunk[c]);
@@ -1101,6 +1103,58 @@ hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, v
   st = launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream);
   if (st != HD_OK) return st;
   return debug_finish(&m, 1, (cudaStream_t)stream);
+}
+
+// Face-centric loop comparison path (hd_fcl.cu).
+hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double t, void *stream) {
+  (void)t;
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_vec(u, "u");
+  if (st == HD_OK) st = check_vec(v, "v");
+  if (st != HD_OK) return st;
+  if (overlaps(u, v, (size_t)m->owned_dofs * sizeof(double))) return fail(HD_ERR_ARG, "u and v overlap");
+  if (m->desc.nranks > 1) return fail(HD_ERR_UNSUPPORTED, "the FCL path is built for single-rank meshes only");
+  if (!hd::fcl_supported(m->d, m->n)) return fail(HD_ERR_UNSUPPORTED, "(d=%d, n=%d) cell does not fit the FCL kernel", m->d, m->n);
+  const long long fn = m->nd / m->n;
+  if (!m->fcl_tr) {
+    const size_t tb = (size_t)2 * m->d * m->ncells_local * fn * sizeof(double);
+    const size_t gb = (size_t)m->d * m->ncells_local * fn * sizeof(double);
+    cudaError_t e = cudaMalloc(&m->fcl_tr, tb);
+    if (e == cudaSuccess) e = cudaMalloc(&m->fcl_G, gb);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (m->fcl_tr) cudaFree(m->fcl_tr);
+      m->fcl_tr = nullptr;
+      m->fcl_G = nullptr;
+      return fail(HD_ERR_OOM, "FCL face buffers (%zu + %zu bytes): %s", tb, gb, cudaGetErrorString(e));
+    }
+  }
+  hd::FclParams p{};
+  p.u = u;
+  p.v = v;
+  p.tr = m->fcl_tr;
+  p.G = m->fcl_G;
+  p.ncells = m->ncells_local;
+  for (int i = 0; i < m->d; ++i) {
+    p.L[i] = m->desc.cells[i];
+    p.L32[i] = (unsigned)m->desc.cells[i];
+    p.lo[i] = m->desc.lo[i];
+    p.h[i] = m->h[i];
+    p.jdet_h[i] = m->jdet / m->h[i];
+    p.a_const[i] = m->desc.a_const[i];
+    for (int j = 0; j < m->d; ++j) p.a_lin[i][j] = m->desc.a_lin[6 * i + j];
+  }
+  for (int a = 0; a < m->n; ++a) {
+    p.xi[a] = m->tab.xi[a];
+    p.w[a] = m->tab.w[a];
+    p.l0[a] = m->tab.tau[1][a];  // tau[1] = l_q(0)
+    p.l1[a] = m->tab.tau[0][a];  // tau[0] = l_q(1)
+    for (int q = 0; q < m->n; ++q) p.Dw[a][q] = m->tab.Dw[a][q];
+  }
+  p.flux = m->desc.flux;
+  cudaError_t e = hd::launch_fcl(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->sms);
+  if (e != cudaSuccess) return cuda_fail(e, "FCL kernels");
+  return HD_OK;
 }
 
 hd_status hd_rk_step(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {

@@ -26,6 +26,7 @@ struct Tables1D {
   double K[2][kMaxN][kMaxN];
   double lam[2][kMaxN];
   double tau[2][kMaxN];
+  double Dw[kMaxN][kMaxN];   // w_q l'_m(xi_q): the unscaled weak volume derivative (FCL path)
 };
 
 // Host-side computation of the tables (independent of the oracle).
@@ -160,6 +161,26 @@ struct FillParams {
   unsigned long long seed;
 };
 
+// Face-centric loop (FCL) comparison path of v <- A(u) (hd_fcl.cu).
+struct FclParams {
+  const double *u;
+  double *v;
+  double *tr;             // [d][2][ncells][n^(d-1)]: face traces u(xi_i = side)
+  double *G;              // [d][ncells][n^(d-1)]: flux of the face (cell, cell + e_i) times |J|/h_i w_f
+  long long ncells;
+  long long L[kMaxD];     // cells per dim (single rank: the global grid)
+  unsigned L32[kMaxD];    // the same as 32-bit divisors (cell indices fit 31 bits)
+  double lo[kMaxD], h[kMaxD], jdet_h[kMaxD];  // jdet_h[i] = |J| / h_i
+  double a_const[kMaxD];
+  double a_lin[kMaxD][kMaxD];
+  double xi[kMaxN], w[kMaxN], l0[kMaxN], l1[kMaxN];
+  double Dw[kMaxN][kMaxN];  // w_q l'_m(xi_q)
+  int flux;               // 0 upwind, 1 central
+};
+bool fcl_supported(int d, int n);
+// three launches (cell, face, lift); *launches += 3
+cudaError_t launch_fcl(int d, int n, const FclParams &p, cudaStream_t s, long long *launches, int sms);
+
 // Launchers (hd_kernels.cu). Return cudaError_t of the launch; *launches incremented.
 cudaError_t upload_tables(int n, const Tables1D &t);
 cudaError_t launch_cell_kernel(int d, int n, const CellParams &p, cudaStream_t s, long long *launches, int grid);
@@ -241,4 +262,5 @@ struct hd_mesh {
   int *pack_cells, *pack_dimsg;
   double *sendbuf;
   void *nccl_comm;         // ncclComm_t when the NCCL transport is used
+  double *fcl_tr, *fcl_G;  // FCL comparison path buffers (allocated by the first hd_apply_advection_fcl)
 };

@@ -96,10 +96,12 @@ void build_tables(int n, Tables1D &t) {
       t.lam[s][m] = 0;
       t.tau[s][m] = 0;
       for (int q = 0; q < kMaxN; ++q) t.K[s][m][q] = 0;
+      for (int q = 0; q < kMaxN && s == 0; ++q) t.Dw[m][q] = 0;
     }
   for (int m = 0; m < n; ++m) {
     for (int q = 0; q < n; ++q) {
       R vol = w01[q] * lag_d(x01, n, m, x01[q]);
+      t.Dw[m][q] = (double)vol;
       t.K[0][m][q] = (double)((vol - l1[m] * l1[q]) / w01[m]);
       t.K[1][m][q] = (double)((vol + l0[m] * l0[q]) / w01[m]);
     }
