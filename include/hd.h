@@ -108,6 +108,24 @@ hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, v
  * otherwise). Three kernel launches on stream. */
 hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double t, void *stream);
 
+/* Vlasov-Poisson (Eq. equ:vp:close; DESIGN.md §6 "Vlasov-Poisson"). A mesh
+ * with d_x = d_v <= 3, one rank, whose field holds the x part a_i = v_i (a_lin[i][d_x + i] = 1); the v part of
+ * the phase-space field is a_{d_x+l} = (desc field) - E_l(x), composed on the fly from an E table at the x
+ * Gauss nodes. Errors as hd_apply_advection_fcl; HD_ERR_UNSUPPORTED for other meshes.
+ *
+ * hd_vp_fields: rho(x) = 1 - int f dv at every x node and E = -grad phi with -lap phi = rho on the
+ *   periodic x box, solved spectrally (SPEC S:567-575 substitute for the paper's multigrid, reading C24):
+ *   rhohat(m) = |Omega_x|^-1 (Gauss rule of rho_h e^{-i k.x}), |m_i| <= (cells_i - 1)/2, zero mode dropped.
+ *   f: device vector of owned_dofs doubles. rho (ncx * n^d_x doubles, [x cell][x node], may be NULL) and
+ *   E (d_x * ncx * n^d_x doubles, [component][x cell][x node], may be NULL): device outputs.
+ * hd_apply_advection_vp: v <- A(u) (weak form) with a = (v, -E(x)) through the face-centric loop (the
+ *   sign of -E changes inside cells, which the upwind ECL kernel does not allow, reading C11). E as above.
+ * hd_vp_rk_step: nsteps LSRK(5,4) steps of df/dt = M^-1 A(f; E(f)) with E recomputed from every stage's f
+ *   (S:577). buf[0] = f (updated in place), buf[1], buf[2] scratch: three distinct device vectors. */
+hd_status hd_vp_fields(hd_mesh *m, const double *f, double *rho, double *E, void *stream);
+hd_status hd_apply_advection_vp(hd_mesh *m, const double *u, const double *E, double *v, void *stream);
+hd_status hd_vp_rk_step(hd_mesh *m, double *buf[3], double t, double dt, int nsteps, void *stream);
+
 /* u <- M^-1 u and u <- M u, in place; one streaming pass, no communication. */
 hd_status hd_apply_inv_mass(hd_mesh *m, double *u, void *stream);
 hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream);

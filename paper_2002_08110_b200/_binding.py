@@ -33,7 +33,7 @@ class HdMeshDesc(ctypes.Structure):
 _lib = None
 
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection", "hd_apply_advection_fcl",
+EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection", "hd_apply_advection_fcl", "hd_vp_fields", "hd_apply_advection_vp", "hd_vp_rk_step",
            "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_stage", "hd_rk_step_host", "hd_apply_advection_group",
            "hd_rk_step_group", "hd_fill_initial", "hd_tables_1d", "hd_lsrk_coefficients", "hd_mesh_traces",
            "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_halo_chunks", "hd_launch_count", "hd_last_error"]
@@ -54,6 +54,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_mesh_info.argtypes = [vp, P(ll), P(ll), P(ll)]
     lib.hd_apply_advection.argtypes = [vp, vp, vp, ctypes.c_double, vp]
     lib.hd_apply_advection_fcl.argtypes = [vp, vp, vp, ctypes.c_double, vp]
+    lib.hd_vp_fields.argtypes = [vp, vp, vp, vp, vp]
+    lib.hd_apply_advection_vp.argtypes = [vp, vp, vp, vp, vp]
+    lib.hd_vp_rk_step.argtypes = [vp, P(vp), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
     lib.hd_apply_inv_mass.argtypes = [vp, vp, vp]
     lib.hd_apply_mass.argtypes = [vp, vp, vp]
     lib.hd_rk_step.argtypes = [vp, P(vp), P(ctypes.c_int), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
@@ -237,6 +240,42 @@ class Mesh:
         _check(load_library().hd_apply_advection_fcl(self._h, self._vec(u, "u"), self._vec(v, "v"), float(t),
                                                      _stream_handle(stream)))
         return v
+
+    def _field(self, x, count, name):
+        import torch
+        if x is None:
+            return None
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+                and x.numel() == count):
+            raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of {count} elements")
+        return ctypes.c_void_p(x.data_ptr())
+
+    def vp_sizes(self):
+        """(x nodes = ncx * n^d_x, E doubles = d_x * x nodes) of a Vlasov-Poisson mesh."""
+        n = self.spec["k"] + 1
+        nxn = 1
+        for c in self.spec["cells"][: self.spec["d_x"]]:
+            nxn *= c * n
+        return nxn, self.spec["d_x"] * nxn
+
+    def vp_fields(self, f, rho=None, E=None, stream=None):
+        """rho = 1 - int f dv and E = -grad phi at the x nodes (hd.h hd_vp_fields)."""
+        nxn, ne = self.vp_sizes()
+        _check(load_library().hd_vp_fields(self._h, self._vec(f, "f"), self._field(rho, nxn, "rho"),
+                                           self._field(E, ne, "E"), _stream_handle(stream)))
+        return rho, E
+
+    def apply_advection_vp(self, u, E, v, stream=None):
+        """v <- A(u) with a = (v, -E(x)) (hd.h hd_apply_advection_vp)."""
+        _check(load_library().hd_apply_advection_vp(self._h, self._vec(u, "u"), self._field(E, self.vp_sizes()[1], "E"),
+                                                    self._vec(v, "v"), _stream_handle(stream)))
+        return v
+
+    def vp_rk_step(self, bufs, t: float, dt: float, nsteps: int = 1, stream=None):
+        """nsteps Vlasov-Poisson LSRK(5,4) steps; bufs[0] = f updated in place (hd.h hd_vp_rk_step)."""
+        arr = (ctypes.c_void_p * 3)(*[self._vec(b, "buf") for b in bufs])
+        _check(load_library().hd_vp_rk_step(self._h, arr, float(t), float(dt), int(nsteps), _stream_handle(stream)))
+        return bufs[0]
 
     def apply_inv_mass(self, u, stream=None):
         _check(load_library().hd_apply_inv_mass(self._h, self._vec(u, "u"), _stream_handle(stream)))

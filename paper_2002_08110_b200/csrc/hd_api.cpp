@@ -209,6 +209,9 @@ void free_mesh(hd_mesh *m) {
   if (m->sendbuf) cudaFree(m->sendbuf);
   if (m->fcl_tr) cudaFree(m->fcl_tr);
   if (m->fcl_G) cudaFree(m->fcl_G);
+  if (m->vp_rho) cudaFree(m->vp_rho);
+  if (m->vp_rhohat) cudaFree(m->vp_rhohat);
+  if (m->vp_E) cudaFree(m->vp_E);
   if (m->nccl_comm && g_nccl.ok) g_nccl.comm_destroy(m->nccl_comm);
   for (int c = 0; c < hd::kMaxChunk; ++c)
     if (m->ev_chunk[c]) cudaEventDestroy(m->ev_chunk[c]);
@@ -1085,29 +1088,7 @@ hd_status check_bufs(hd_mesh *m, double *buf[3], int *sol, int nsteps, double dt
 
 }  // namespace
 
-extern "C" {
-
-hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream) {
-  (void)t;
-  if (!m) return fail(HD_ERR_ARG, "null argument");
-  hd_status st = check_vec(u, "u");
-  if (st == HD_OK) st = check_vec(v, "v");
-  if (st != HD_OK) return st;
-  if (overlaps(u, v, (size_t)m->owned_dofs * sizeof(double))) return fail(HD_ERR_ARG, "u and v overlap");
-  st = check_transport(m);
-  if (st == HD_OK) st = ensure_tables(m);
-  if (st != HD_OK) return st;
-  hd::CellParams p;
-  fill_cell_params(m, p);
-  set_dtfac(m, p, 1.0);
-  st = launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream);
-  if (st != HD_OK) return st;
-  return debug_finish(&m, 1, (cudaStream_t)stream);
-}
-
-// Face-centric loop comparison path (hd_fcl.cu; SURVEY §8(f) NEXT-3, P:579-600, P:3077).
-hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double t, void *stream) {
-  (void)t;
+static hd_status fcl_impl(hd_mesh *m, const double *u, double *v, const double *E, void *stream) {
   if (!m) return fail(HD_ERR_ARG, "null argument");
   hd_status st = check_vec(u, "u");
   if (st == HD_OK) st = check_vec(v, "v");
@@ -1152,8 +1133,151 @@ hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double 
     for (int q = 0; q < m->n; ++q) p.Dw[a][q] = m->tab.Dw[a][q];
   }
   p.flux = m->desc.flux;
+  p.E = E;
+  p.d_x = m->desc.d_x;
+  p.ncx = m->cx_total;
+  p.nx = 1;
+  for (int i = 0; i < m->desc.d_x; ++i) p.nx *= m->n;
   cudaError_t e = hd::launch_fcl(m->d, m->n, p, (cudaStream_t)stream, &m->launches, m->sms);
   if (e != cudaSuccess) return cuda_fail(e, "FCL kernels");
+  return HD_OK;
+}
+
+extern "C" {
+
+hd_status hd_apply_advection(hd_mesh *m, const double *u, double *v, double t, void *stream) {
+  (void)t;
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_vec(u, "u");
+  if (st == HD_OK) st = check_vec(v, "v");
+  if (st != HD_OK) return st;
+  if (overlaps(u, v, (size_t)m->owned_dofs * sizeof(double))) return fail(HD_ERR_ARG, "u and v overlap");
+  st = check_transport(m);
+  if (st == HD_OK) st = ensure_tables(m);
+  if (st != HD_OK) return st;
+  hd::CellParams p;
+  fill_cell_params(m, p);
+  set_dtfac(m, p, 1.0);
+  st = launch_stage(m, p, u, nullptr, v, hd::kModeAdvection, 0.0, 0.0, (cudaStream_t)stream);
+  if (st != HD_OK) return st;
+  return debug_finish(&m, 1, (cudaStream_t)stream);
+}
+
+// Face-centric loop comparison path (hd_fcl.cu; SURVEY §8(f) NEXT-3, P:579-600, P:3077).
+hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double t, void *stream) {
+  (void)t;
+  return fcl_impl(m, u, v, nullptr, stream);
+}
+
+// Vlasov-Poisson (hd_fcl.cu, Eq. equ:vp:close; DESIGN.md §6 "Vlasov-Poisson")
+static hd_status vp_setup(hd_mesh *m, hd::VpParams &vp) {
+  const int dx = m->desc.d_x, dv = m->desc.d_v, n = m->n;
+  if (m->desc.nranks > 1) return fail(HD_ERR_UNSUPPORTED, "the Vlasov-Poisson path is built for single-rank meshes only");
+  if (dx != dv || dx > 3) return fail(HD_ERR_UNSUPPORTED, "Vlasov-Poisson needs d_x = d_v <= 3");
+  vp = hd::VpParams{};
+  vp.d_x = dx;
+  vp.n = n;
+  vp.nx = 1;
+  vp.nv = 1;
+  for (int i = 0; i < dx; ++i) vp.nx *= n;
+  for (int i = 0; i < dv; ++i) vp.nv *= n;
+  if (vp.nv > 216) return fail(HD_ERR_UNSUPPORTED, "too many v nodes per cell");
+  vp.ND = (int)m->nd;
+  vp.ncx = m->cx_total;
+  vp.ncv = m->ncells_local / m->cx_total;
+  vp.vol_x = 1.0;
+  vp.nmodes = 1;
+  for (int i = 0; i < dx; ++i) {
+    vp.Lx[i] = m->desc.cells[i];
+    vp.lo[i] = m->desc.lo[i];
+    vp.h[i] = m->h[i];
+    vp.Lbox[i] = m->desc.hi[i] - m->desc.lo[i];
+    vp.vol_x *= vp.Lbox[i];
+    vp.K[i] = (m->desc.cells[i] - 1) / 2;  // modes below the per-cell Nyquist phase (reading C24)
+    vp.nmodes *= 2 * vp.K[i] + 1;
+  }
+  for (int a = 0; a < n; ++a) {
+    vp.xi[a] = m->tab.xi[a];
+    vp.w[a] = m->tab.w[a];
+  }
+  for (int jv = 0; jv < vp.nv; ++jv) {
+    double w = 1.0;
+    int r = jv;
+    for (int i = 0; i < dv; ++i) {
+      w *= m->tab.w[r % n] * m->h[dx + i];
+      r /= n;
+    }
+    vp.wv[jv] = w;
+  }
+  if (!m->vp_rho) {
+    const size_t nxn = (size_t)vp.ncx * vp.nx;
+    cudaError_t e = cudaMalloc(&m->vp_rho, nxn * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&m->vp_rhohat, (size_t)2 * vp.nmodes * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&m->vp_E, (size_t)dx * nxn * sizeof(double));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HD_ERR_OOM, "Vlasov-Poisson field buffers: %s", cudaGetErrorString(e));
+    }
+  }
+  return ensure_tables(m);
+}
+
+hd_status hd_vp_fields(hd_mesh *m, const double *f, double *rho, double *E, void *stream) {
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_vec(f, "f");
+  if (st != HD_OK) return st;
+  hd::VpParams vp;
+  st = vp_setup(m, vp);
+  if (st != HD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = hd::launch_vp_fields(vp, f, m->vp_rho, m->vp_rhohat, m->vp_E, s, &m->launches, m->sms);
+  const size_t nxn = (size_t)vp.ncx * vp.nx;
+  if (e == cudaSuccess && rho) e = cudaMemcpyAsync(rho, m->vp_rho, nxn * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && E) e = cudaMemcpyAsync(E, m->vp_E, vp.d_x * nxn * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "Vlasov-Poisson fields");
+  return HD_OK;
+}
+
+hd_status hd_apply_advection_vp(hd_mesh *m, const double *u, const double *E, double *v, void *stream) {
+  if (!m || !E) return fail(HD_ERR_ARG, "null argument");
+  if (m->desc.d_x != m->desc.d_v) return fail(HD_ERR_UNSUPPORTED, "Vlasov-Poisson needs d_x = d_v");
+  return fcl_impl(m, u, v, E, stream);
+}
+
+hd_status hd_vp_rk_step(hd_mesh *m, double *buf[3], double t, double dt, int nsteps, void *stream) {
+  (void)t;
+  if (!m || !buf) return fail(HD_ERR_ARG, "null argument");
+  if (nsteps < 1 || !std::isfinite(dt)) return fail(HD_ERR_ARG, "nsteps must be >= 1 and dt finite");
+  const size_t bytes = (size_t)m->owned_dofs * sizeof(double);
+  for (int i = 0; i < 3; ++i) {
+    hd_status st = check_vec(buf[i], "buf");
+    if (st != HD_OK) return st;
+    for (int j = 0; j < i; ++j)
+      if (overlaps(buf[i], buf[j], bytes)) return fail(HD_ERR_ARG, "buffers overlap");
+  }
+  hd::VpParams vp;
+  hd_status st = vp_setup(m, vp);
+  if (st != HD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  hd::StreamParams mp;
+  mp.u = buf[2];
+  mp.ndofs = m->owned_dofs;
+  mp.jdet = m->jdet;
+  mp.inverse = 1;
+  for (int step = 0; step < nsteps; ++step) {
+    for (int stage = 0; stage < 5; ++stage) {
+      // E(t_s) from the stage's f ("recomputed once per RK stage"), then M^-1 A(f; a = (v, -E))
+      cudaError_t e = hd::launch_vp_fields(vp, buf[0], m->vp_rho, m->vp_rhohat, m->vp_E, s, &m->launches, m->sms);
+      if (e != cudaSuccess) return cuda_fail(e, "Vlasov-Poisson fields");
+      st = fcl_impl(m, buf[0], buf[2], m->vp_E, stream);
+      if (st != HD_OK) return st;
+      e = hd::launch_mass_kernel(m->d, m->n, mp, s, &m->launches, m->sms);
+      if (e == cudaSuccess)
+        e = hd::launch_vp_update(buf[0], buf[1], buf[2], m->owned_dofs, kRkA[stage], kRkB[stage], dt, stage == 0, s,
+                                 &m->launches, m->sms);
+      if (e != cudaSuccess) return cuda_fail(e, "Vlasov-Poisson stage");
+    }
+  }
   return HD_OK;
 }
 

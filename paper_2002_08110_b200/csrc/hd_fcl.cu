@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(256) fcl_cell_kernel(const __grid_constant__ F
           a += p.a_lin[i][j] * (p.lo[j] + ((double)cc[j] + p.xi[mi[j]]) * p.h[j]);
           wf *= p.w[mi[j]];
         }
+        // Vlasov-Poisson: a_{d_x + l} = ... - E_l(x) at the DoF's x node (P:3963 a = (v, -E(x)))
+        if (p.E && i >= p.d_x) a -= p.E[((long long)(i - p.d_x) * p.ncx + cell % p.ncx) * p.nx + m % p.nx];
         int stride = 1;
         for (int j = 0; j < i; ++j) stride *= N;
         const int base = m - mi[i] * stride;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(256) fcl_face_kernel(const __grid_constant__ F
         wf *= p.w[mj];
       }
     }
+    if (p.E && i >= p.d_x) a -= p.E[((long long)(i - p.d_x) * p.ncx + cell % p.ncx) * p.nx + f % p.nx];
     const unsigned right = ci + 1 < p.L32[i] ? cell + csi : cell - (p.L32[i] - 1) * csi;  // periodic
     const double um = p.tr[((long long)(2 * i + 1) * p.ncells + cell) * FN + f];
     const double up = p.tr[((long long)(2 * i) * p.ncells + right) * FN + f];
@@ -206,7 +209,163 @@ cudaError_t launch_fcl_dn(const FclParams &p, cudaStream_t s, int sms) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Vlasov-Poisson (Eq. equ:vp:close; DESIGN.md §6 "Vlasov-Poisson").
+// rho(x) = 1 - int f dv at every x node: one CTA per x cell; thread e of the cell-local index sums
+// its value over the v cells (coalesced: consecutive threads, consecutive DoFs), then the x nodes sum their
+// v nodes from shared memory. Fixed summation order (deterministic).
+__global__ void __launch_bounds__(256) vp_density_kernel(const __grid_constant__ VpParams p, const double *f,
+                                                         double *rho) {
+  extern __shared__ double S[];  // [ND]
+  for (long long cx = blockIdx.x; cx < p.ncx; cx += gridDim.x) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < p.ND; e += blockDim.x) {
+      const double *fc = f + cx * p.ND + e;
+      double s = 0.0;
+      for (long long cv = 0; cv < p.ncv; ++cv) s += __ldcs(fc + cv * p.ncx * p.ND);
+      S[e] = p.wv[e / p.nx] * s;
+    }
+    __syncthreads();
+    for (int jx = threadIdx.x; jx < p.nx; jx += blockDim.x) {
+      double s = 0.0;
+      for (int jv = 0; jv < p.nv; ++jv) s += S[jx + jv * p.nx];
+      rho[cx * p.nx + jx] = 1.0 - s;
+    }
+  }
+}
+
+// x-node coordinates of (x cell cx, x node jx)
+__device__ __forceinline__ void vp_xnode(const VpParams &p, long long cx, int jx, double *x, double *w) {
+  double ww = 1.0;
+  for (int i = 0; i < p.d_x; ++i) {
+    const long long c = cx % p.Lx[i];
+    cx /= p.Lx[i];
+    const int j = jx % p.n;
+    jx /= p.n;
+    x[i] = p.lo[i] + ((double)c + p.xi[j]) * p.h[i];
+    ww *= p.w[j] * p.h[i];
+  }
+  *w = ww;
+}
+
+// Fourier coefficients of rho_h by its Gauss rule: rhohat(m) = |Omega_x|^-1 sum_nodes W rho e^{-i k.x},
+// k_i = 2 pi m_i / L_i, |m_i| <= K_i: one CTA per mode, threads over the x nodes, fixed-shape tree reduction
+// in shared memory (deterministic).
+__global__ void __launch_bounds__(256) vp_rhohat_kernel(const __grid_constant__ VpParams p, const double *rho,
+                                                        double *rhohat) {
+  __shared__ double sre[256], sim[256];
+  for (long long q = blockIdx.x; q < p.nmodes; q += gridDim.x) {
+    double k[3] = {0, 0, 0};
+    long long r = q;
+    for (int i = 0; i < p.d_x; ++i) {
+      const long long w = 2 * p.K[i] + 1;
+      k[i] = 2.0 * M_PI * (double)(r % w - p.K[i]) / p.Lbox[i];
+      r /= w;
+    }
+    double re = 0.0, im = 0.0;
+    const long long nxn = p.ncx * p.nx;
+    for (long long e = threadIdx.x; e < nxn; e += blockDim.x) {
+      const long long cx = e / p.nx;
+      double x[3], W;
+      vp_xnode(p, cx, (int)(e - cx * p.nx), x, &W);
+      double ph = 0.0;
+      for (int i = 0; i < p.d_x; ++i) ph += k[i] * x[i];
+      double sn, cs;
+      sincos(ph, &sn, &cs);
+      const double t = W * rho[e];
+      re += t * cs;
+      im -= t * sn;
+    }
+    __syncthreads();
+    sre[threadIdx.x] = re;
+    sim[threadIdx.x] = im;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+      if (threadIdx.x < h) {
+        sre[threadIdx.x] += sre[threadIdx.x + h];
+        sim[threadIdx.x] += sim[threadIdx.x + h];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      rhohat[2 * q] = sre[0] / p.vol_x;
+      rhohat[2 * q + 1] = sim[0] / p.vol_x;
+    }
+  }
+}
+
+// E = -grad phi, -lap phi = rho: E_i(x) = sum_{m != 0} k_i / |k|^2 (Re rhohat sin(k.x) + Im rhohat cos(k.x)),
+// at every x node: thread per (x cell, x node); out E[i][cx][jx].
+__global__ void __launch_bounds__(256) vp_efield_kernel(const __grid_constant__ VpParams p, const double *rhohat,
+                                                        double *E) {
+  const long long nxn = p.ncx * p.nx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nxn; e += (long long)gridDim.x * blockDim.x) {
+    const long long cx = e / p.nx;
+    double x[3], W;
+    vp_xnode(p, cx, (int)(e - cx * p.nx), x, &W);
+    double acc[3] = {0, 0, 0};
+    for (long long q = 0; q < p.nmodes; ++q) {
+      double k[3] = {0, 0, 0}, k2 = 0.0;
+      long long r = q;
+      for (int i = 0; i < p.d_x; ++i) {
+        const long long w = 2 * p.K[i] + 1;
+        k[i] = 2.0 * M_PI * (double)(r % w - p.K[i]) / p.Lbox[i];
+        k2 += k[i] * k[i];
+        r /= w;
+      }
+      if (k2 == 0.0) continue;
+      double ph = 0.0;
+      for (int i = 0; i < p.d_x; ++i) ph += k[i] * x[i];
+      double sn, cs;
+      sincos(ph, &sn, &cs);
+      const double g = rhohat[2 * q] * sn + rhohat[2 * q + 1] * cs;
+      for (int i = 0; i < p.d_x; ++i) acc[i] += k[i] / k2 * g;
+    }
+    for (int i = 0; i < p.d_x; ++i) E[(long long)i * nxn + e] = acc[i];
+  }
+}
+
+// 2N low-storage update of one stage: dU <- A_s dU + dt w (first stage: dU <- dt w); U <- U + B_s dU
+__global__ void __launch_bounds__(256) vp_update_kernel(double *U, double *dU, const double *w, long long n, double A,
+                                                        double B, double dt, int first) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const double d = first ? dt * w[e] : A * dU[e] + dt * w[e];
+    dU[e] = d;
+    U[e] = U[e] + B * d;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_vp_fields(const VpParams &p, const double *f, double *rho, double *rhohat, double *E, cudaStream_t s,
+                             long long *launches, int sms) {
+  const long long nxn = p.ncx * p.nx;
+  const long long cap = (long long)sms * 16;
+  auto grid = [&](long long n) { long long g = (n + 255) / 256; return (unsigned)(g < 1 ? 1 : (g < cap ? g : cap)); };
+  const size_t smem = (size_t)p.ND * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(vp_density_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  vp_density_kernel<<<(unsigned)(p.ncx < cap ? p.ncx : cap), 256, smem, s>>>(p, f, rho);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  vp_rhohat_kernel<<<(unsigned)(p.nmodes < cap ? p.nmodes : cap), 256, 0, s>>>(p, rho, rhohat);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  vp_efield_kernel<<<grid(nxn), 256, 0, s>>>(p, rhohat, E);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vp_update(double *U, double *dU, const double *w, long long n, double A, double B, double dt,
+                             int first, cudaStream_t s, long long *launches, int sms) {
+  long long g = (n + 255) / 256;
+  const long long cap = (long long)sms * 16;
+  if (g > cap) g = cap;
+  if (g < 1) return cudaSuccess;
+  vp_update_kernel<<<(unsigned)g, 256, 0, s>>>(U, dU, w, n, A, B, dt, first);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
 
 bool fcl_supported(int d, int n) {
   if (d < 2 || d > 6 || n < 2 || n > 6) return false;

@@ -176,7 +176,26 @@ struct FclParams {
   double xi[kMaxN], w[kMaxN], l0[kMaxN], l1[kMaxN];
   double Dw[kMaxN][kMaxN];  // w_q l'_m(xi_q)
   int flux;               // 0 upwind, 1 central
+  // Vlasov-Poisson (NEXT-1): when E is set, a_{d_x + l} -= E[l][x cell][x node] (P:3963 a = (v, -E(x)))
+  const double *E;
+  int d_x;
+  long long ncx;          // x cells (the flat x-cell index is cell % ncx: x dims are the fastest)
+  int nx;                 // n^d_x x nodes per x cell
 };
+// Vlasov-Poisson field pipeline (hd_fcl.cu): rho = 1 - int f dv, its Fourier coefficients, E = -grad phi
+struct VpParams {
+  int d_x, n, nx, nv, ND;     // nx = n^d_x, nv = n^d_v, ND = n^d
+  long long ncx, ncv;         // x cells, v cells
+  long long Lx[3];            // x cells per x dim
+  double lo[3], h[3], Lbox[3], xi[kMaxN], w[kMaxN];
+  double vol_x;               // |Omega_x|
+  long long K[3], nmodes;     // modes |m_i| <= K_i, prod (2 K_i + 1)
+  double wv[216];             // per v node: prod w_{j_v} h_v (|J_v| times the v quadrature weight)
+};
+cudaError_t launch_vp_fields(const VpParams &p, const double *f, double *rho, double *rhohat, double *E, cudaStream_t s,
+                             long long *launches, int sms);
+cudaError_t launch_vp_update(double *U, double *dU, const double *w, long long n, double A, double B, double dt,
+                             int first, cudaStream_t s, long long *launches, int sms);
 bool fcl_supported(int d, int n);
 // three launches (cell, face, lift); *launches += 3
 cudaError_t launch_fcl(int d, int n, const FclParams &p, cudaStream_t s, long long *launches, int sms);
@@ -263,4 +282,5 @@ struct hd_mesh {
   double *sendbuf;
   void *nccl_comm;         // ncclComm_t when the NCCL transport is used
   double *fcl_tr, *fcl_G;  // FCL comparison path buffers (allocated by the first hd_apply_advection_fcl)
+  double *vp_rho, *vp_rhohat, *vp_E;  // Vlasov-Poisson field buffers (allocated by the first hd_vp_* call)
 };
