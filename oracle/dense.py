@@ -56,8 +56,10 @@ def _speed(spec, i, Z):
     return a
 
 
-def assemble(spec: dict, over: int = 2):
-    """Return dense (A, M) in global DoF order (reading C19)."""
+def assemble(spec: dict, over: int = 2, nodes=None):
+    """Return dense (A, M) in global DoF order (reading C19). ``nodes``: the 1D interpolation nodes on
+    [0, 1] of the nodal basis (default: the n Gauss points, reading C1; oracle/gll.py passes the
+    Gauss-Lobatto points of the paper's default basis)."""
     d = spec["d_x"] + spec["d_v"]
     n = spec["k"] + 1
     cells = [int(c) for c in spec["cells"]]
@@ -67,7 +69,10 @@ def assemble(spec: dict, over: int = 2):
     ncell = int(np.prod(cells))
     N = ncell * nd
     flux = spec.get("flux", "upwind")
-    nodes, _ = _gl01(n)
+    if nodes is None:
+        nodes, _ = _gl01(n)
+    nodes = np.asarray(nodes, float)
+    assert nodes.shape == (n,)
     xq, wq = _gl01(n + over)
     B, G = _lagrange_matrix(nodes, xq)           # [nq, n]
     b0, _ = _lagrange_matrix(nodes, np.array([0.0]))
