@@ -363,6 +363,25 @@ def run_gpu(args):
             else:
                 extra["apply_advection_fcl"] = {"skipped": f"face buffers ({fcl_bytes / 1e9:.1f} GB) do not fit the "
                                                            f"{free / 1e9:.1f} GB left beside the product path's buffers"}
+        # the GLL <-> Gauss basis change (hd_basis_change, "quantify the overhead
+        # resulting from the basis change") alone (16 B/DoF) and around the operator (T, A, T^T: 3 launches)
+        try:
+            for _ in range(2):
+                mesh.basis_change(u, v, "gll_to_gauss", stream)
+            barrier()
+            b_ms = timed(lambda: mesh.basis_change(u, v, "gll_to_gauss", stream), reps) / reps
+            b_gdofs = ndofs / (b_ms * 1e-3) / 1e9
+            for _ in range(2):
+                mesh.apply_advection_gll(u, v, w, 0.0, stream)
+            barrier()
+            g_ms = timed(lambda: mesh.apply_advection_gll(u, v, w, 0.0, stream), reps) / reps
+            extra["basis_change"] = {"gdofs": b_gdofs, "ms": b_ms,
+                                     "roofline": op_roofline(b_gdofs, "basis_kernel (v <- (T x ... x T) u per cell)", "basis")}
+            extra["apply_advection_gll"] = {"gdofs": ndofs / (g_ms * 1e-3) / 1e9, "ms": g_ms,
+                                            "overhead_vs_gauss_collocation": g_ms / a_ms,
+                                            "launches": "basis_kernel(T) + cell_kernel<A> + basis_kernel(T^T)"}
+        except Exception as ex:  # noqa: BLE001 -- (d, n) whose cell does not fit the basis kernel
+            extra["basis_change"] = {"skipped": str(ex)}
         # keep the solution buffer intact for e2e: u, v, w are distinct
         mesh.fill_initial(bufs[0], cfg["recipe"], seed)
         sol = 0

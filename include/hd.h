@@ -126,6 +126,29 @@ hd_status hd_vp_fields(hd_mesh *m, const double *f, double *rho, double *E, void
 hd_status hd_apply_advection_vp(hd_mesh *m, const double *u, const double *E, double *v, void *stream);
 hd_status hd_vp_rk_step(hd_mesh *m, double *buf[3], double t, double dt, int nsteps, void *stream);
 
+/* GLL nodal basis with Gauss quadrature: the paper's default discretisation and its
+ * basis change ("a sequence of d 1D interpolation sweeps", Cartesian
+ * part; DESIGN.md §6 "Basis change"). T[q][j] = l^GLL_j(xi^Gauss_q), applied along every dim of every cell.
+ * The mesh's own vectors hold Gauss-point values (reading C1); these calls convert at the boundary.
+ *
+ * hd_basis_change: v <- (S x ... x S) u per cell, S by kind. u, v: device vectors of owned_dofs doubles, equal
+ *   (in place) or non-overlapping (HD_ERR_ARG otherwise). Cell-local: any partition. One launch.
+ * hd_apply_advection_gll: v <- A_L u = T^T A_G (T u), the weak form in the GLL basis (P:556-567 steps 1-5).
+ *   work: device scratch of owned_dofs doubles; u, v, work pairwise non-overlapping. Errors as hd_apply_advection.
+ * hd_rk_step_gll: hd_rk_step on GLL coefficients: buf[*sol] is converted to Gauss values in place, stepped,
+ *   and the result converted back (T is constant in time, so no stage needs a basis change).
+ * hd_basis_tables (host): gll[n] = the GLL points on [0,1]; T[4][n][n] = the matrices by kind, [out][in]. */
+typedef enum {
+  HD_GLL_TO_GAUSS = 0,   /* T       : GLL coefficients -> values at the Gauss points */
+  HD_GAUSS_TO_GLL = 1,   /* T^-1    : Gauss values -> GLL coefficients */
+  HD_GLL_TO_GAUSS_T = 2, /* T^T     : Gauss-basis weak form (test side) -> GLL-basis weak form */
+  HD_GAUSS_TO_GLL_T = 3  /* T^-T */
+} hd_basis_kind;
+hd_status hd_basis_change(hd_mesh *m, const double *u, double *v, int kind, void *stream);
+hd_status hd_apply_advection_gll(hd_mesh *m, const double *u, double *v, double *work, double t, void *stream);
+hd_status hd_rk_step_gll(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream);
+hd_status hd_basis_tables(int n, double *gll, double *T);
+
 /* u <- M^-1 u and u <- M u, in place; one streaming pass, no communication. */
 hd_status hd_apply_inv_mass(hd_mesh *m, double *u, void *stream);
 hd_status hd_apply_mass(hd_mesh *m, double *u, void *stream);

@@ -34,6 +34,7 @@ _lib = None
 
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hd_create_mesh", "hd_destroy_mesh", "hd_mesh_info", "hd_mesh_box", "hd_apply_advection", "hd_apply_advection_fcl", "hd_vp_fields", "hd_apply_advection_vp", "hd_vp_rk_step",
+           "hd_basis_change", "hd_apply_advection_gll", "hd_rk_step_gll", "hd_basis_tables",
            "hd_apply_inv_mass", "hd_apply_mass", "hd_rk_step", "hd_rk_stage", "hd_rk_step_host", "hd_apply_advection_group",
            "hd_rk_step_group", "hd_fill_initial", "hd_tables_1d", "hd_lsrk_coefficients", "hd_mesh_traces",
            "hd_nccl_unique_id", "hd_partition_info", "hd_halo_list", "hd_halo_chunks", "hd_launch_count", "hd_last_error"]
@@ -57,6 +58,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.hd_vp_fields.argtypes = [vp, vp, vp, vp, vp]
     lib.hd_apply_advection_vp.argtypes = [vp, vp, vp, vp, vp]
     lib.hd_vp_rk_step.argtypes = [vp, P(vp), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
+    lib.hd_basis_change.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+    lib.hd_apply_advection_gll.argtypes = [vp, vp, vp, vp, ctypes.c_double, vp]
+    lib.hd_rk_step_gll.argtypes = [vp, P(vp), P(ctypes.c_int), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
+    lib.hd_basis_tables.argtypes = [ctypes.c_int, dp, dp]
     lib.hd_apply_inv_mass.argtypes = [vp, vp, vp]
     lib.hd_apply_mass.argtypes = [vp, vp, vp]
     lib.hd_rk_step.argtypes = [vp, P(vp), P(ctypes.c_int), ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
@@ -175,6 +180,15 @@ def tables_1d(n: int):
     return dict(xi=xi, w=w, K=K, lam=lam, tau=tau)
 
 
+def basis_tables(n: int):
+    """Host-side GLL points and the four basis-change matrices [kind][out][in] (hd.h hd_basis_tables)."""
+    import numpy as np
+    gll, T = np.zeros(n), np.zeros((4, n, n))
+    P = ctypes.POINTER(ctypes.c_double)
+    _check(load_library().hd_basis_tables(n, gll.ctypes.data_as(P), T.ctypes.data_as(P)))
+    return gll, T
+
+
 def lsrk_coefficients():
     import numpy as np
     a, b = np.zeros(5), np.zeros(5)
@@ -290,6 +304,27 @@ class Mesh:
         s = ctypes.c_int(sol)
         _check(load_library().hd_rk_step(self._h, arr, ctypes.byref(s), float(t), float(dt), int(nsteps),
                                          _stream_handle(stream)))
+        return s.value
+
+    BASIS_KINDS = {"gll_to_gauss": 0, "gauss_to_gll": 1, "gll_to_gauss_T": 2, "gauss_to_gll_T": 3}
+
+    def basis_change(self, u, v, kind, stream=None):
+        """v <- (S x ... x S) u per cell (hd.h hd_basis_change); v may be u."""
+        k = self.BASIS_KINDS[kind] if isinstance(kind, str) else int(kind)
+        _check(load_library().hd_basis_change(self._h, self._vec(u, "u"), self._vec(v, "v"), k, _stream_handle(stream)))
+        return v
+
+    def apply_advection_gll(self, u, v, work, t: float = 0.0, stream=None):
+        """v <- T^T A(T u): the weak form in the GLL basis (hd.h hd_apply_advection_gll)."""
+        _check(load_library().hd_apply_advection_gll(self._h, self._vec(u, "u"), self._vec(v, "v"),
+                                                     self._vec(work, "work"), float(t), _stream_handle(stream)))
+        return v
+
+    def rk_step_gll(self, bufs, sol: int, t: float, dt: float, nsteps: int = 1, stream=None) -> int:
+        arr = (ctypes.c_void_p * 3)(*[self._vec(b, f"buf[{i}]").value for i, b in enumerate(bufs)])
+        s = ctypes.c_int(sol)
+        _check(load_library().hd_rk_step_gll(self._h, arr, ctypes.byref(s), float(t), float(dt), int(nsteps),
+                                             _stream_handle(stream)))
         return s.value
 
     def rk_stage(self, U, dU, out, stage: int, dt: float, stream=None):

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhd.so")
-SOURCES = ["hd_api.cpp", "hd_plan.cpp", "hd_sched.cpp", "hd_tables.cpp", "hd_kernels.cu", "hd_fcl.cu"]
+SOURCES = ["hd_api.cpp", "hd_plan.cpp", "hd_sched.cpp", "hd_tables.cpp", "hd_kernels.cu", "hd_fcl.cu", "hd_basis.cu"]
 HEADERS = ["hd_internal.h", "hd_cell.cuh", os.path.join("..", "..", "include", "hd.h")]  # every header the sources include
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

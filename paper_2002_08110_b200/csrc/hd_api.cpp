@@ -1169,6 +1169,82 @@ hd_status hd_apply_advection_fcl(hd_mesh *m, const double *u, double *v, double 
   return fcl_impl(m, u, v, nullptr, stream);
 }
 
+// GLL nodal basis <-> Gauss-point values (hd_basis.cu; SURVEY §8(f) NEXT-2, P:228-233, P:509-518, P:556-574;
+// DESIGN.md §6 "Basis change")
+static hd_status basis_impl(hd_mesh *m, const double *u, double *v, int kind, cudaStream_t s) {
+  if (kind < 0 || kind > 3) return fail(HD_ERR_ARG, "kind must be 0..3 (hd_basis_kind)");
+  if (!hd::basis_kernel_supported(m->d, m->n))
+    return fail(HD_ERR_UNSUPPORTED, "(d=%d, n=%d) cell does not fit the basis-change kernel", m->d, m->n);
+  const size_t bytes = (size_t)m->owned_dofs * sizeof(double);
+  if (u != v && overlaps(u, v, bytes)) return fail(HD_ERR_ARG, "u and v overlap without being equal");
+  double S[4][hd::kMaxN * hd::kMaxN];
+  hd::build_basis_tables(m->n, S);
+  hd::BasisParams p{};
+  p.u = u;
+  p.v = v;
+  p.ncells = m->ncells_local;
+  p.d = m->d;
+  for (int e = 0; e < m->n * m->n; ++e) p.S[e] = S[kind][e];
+  cudaError_t e = hd::launch_basis_kernel(m->n, p, s, &m->launches, m->sms);
+  if (e != cudaSuccess) return cuda_fail(e, "basis change");
+  return HD_OK;
+}
+
+hd_status hd_basis_change(hd_mesh *m, const double *u, double *v, int kind, void *stream) {
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_vec(u, "u");
+  if (st == HD_OK) st = check_vec(v, "v");
+  if (st != HD_OK) return st;
+  return basis_impl(m, u, v, kind, (cudaStream_t)stream);
+}
+
+hd_status hd_apply_advection_gll(hd_mesh *m, const double *u, double *v, double *work, double t, void *stream) {
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_vec(u, "u");
+  if (st == HD_OK) st = check_vec(v, "v");
+  if (st == HD_OK) st = check_vec(work, "work");
+  if (st != HD_OK) return st;
+  const size_t bytes = (size_t)m->owned_dofs * sizeof(double);
+  if (overlaps(u, v, bytes) || overlaps(u, work, bytes) || overlaps(v, work, bytes))
+    return fail(HD_ERR_ARG, "u, v and work overlap");
+  // P:556-567 steps 2-4: interpolate to the Gauss points, the Gauss-point operator, test with the transpose
+  st = basis_impl(m, u, work, HD_GLL_TO_GAUSS, (cudaStream_t)stream);
+  if (st == HD_OK) st = hd_apply_advection(m, work, v, t, stream);
+  if (st == HD_OK) st = basis_impl(m, v, v, HD_GLL_TO_GAUSS_T, (cudaStream_t)stream);
+  return st;
+}
+
+hd_status hd_rk_step_gll(hd_mesh *m, double *buf[3], int *sol, double t, double dt, int nsteps, void *stream) {
+  if (!m) return fail(HD_ERR_ARG, "null argument");
+  hd_status st = check_bufs(m, buf, sol, nsteps, dt);
+  if (st != HD_OK) return st;
+  // T does not depend on time: one basis change in, the Gauss-basis time loop, one basis change out
+  st = basis_impl(m, buf[*sol], buf[*sol], HD_GLL_TO_GAUSS, (cudaStream_t)stream);
+  if (st == HD_OK) st = hd_rk_step(m, buf, sol, t, dt, nsteps, stream);
+  if (st == HD_OK) st = basis_impl(m, buf[*sol], buf[*sol], HD_GAUSS_TO_GLL, (cudaStream_t)stream);
+  return st;
+}
+
+hd_status hd_basis_tables(int n, double *gll, double *T) {
+  if (n < 2 || n > hd::kMaxN) return fail(HD_ERR_ARG, "n must be in 2..%d", hd::kMaxN);
+  double S[4][hd::kMaxN * hd::kMaxN];
+  hd::build_basis_tables(n, S);
+  if (T)
+    for (int k = 0; k < 4; ++k)
+      for (int e = 0; e < n * n; ++e) T[k * n * n + e] = S[k][e];
+  if (gll) {
+    // the GLL points are where the Gauss-to-GLL interpolation of the coordinate x lands
+    hd::Tables1D t;
+    hd::build_tables(n, t);
+    for (int j = 0; j < n; ++j) {
+      double x = 0.0;
+      for (int q = 0; q < n; ++q) x += S[1][j * n + q] * t.xi[q];
+      gll[j] = x;
+    }
+  }
+  return HD_OK;
+}
+
 // Vlasov-Poisson (hd_fcl.cu, Eq. equ:vp:close; DESIGN.md §6 "Vlasov-Poisson")
 static hd_status vp_setup(hd_mesh *m, hd::VpParams &vp) {
   const int dx = m->desc.d_x, dv = m->desc.d_v, n = m->n;

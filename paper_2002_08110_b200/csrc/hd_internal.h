@@ -31,6 +31,17 @@ struct Tables1D {
 
 // Host-side computation of the tables (independent of the oracle).
 void build_tables(int n, Tables1D &t);
+// GLL <-> Gauss basis-change matrices (hd_tables.cpp): [kind][out * n + in], kind as hd_basis_kind
+void build_basis_tables(int n, double S[4][kMaxN * kMaxN]);
+
+// basis_kernel (hd_basis.cu): the 1D matrix S applied along every dim of every cell
+struct BasisParams {
+  const double *u;
+  double *v;
+  long long ncells;
+  int d, cb;                 // dims, cells per CTA batch
+  double S[kMaxN * kMaxN];   // [out * n + in]
+};
 
 enum Mode : int { kModeAdvection = 0, kModeRK = 1, kModeRKFirst = 2, kModeAdvAcc = 3 /* v += A u (central flux) */ };
 
@@ -210,6 +221,8 @@ cudaError_t launch_pack_kernel(int d, int n, const PackParams &pp, const CellPar
 // HD_DEBUG: set bit 4 of *err if any of the n values is not finite
 cudaError_t launch_finite_check(const double *v, long long n, int *err, cudaStream_t s);
 bool cell_kernel_supported(int d, int n);
+cudaError_t launch_basis_kernel(int n, BasisParams &p, cudaStream_t s, long long *launches, int sms);
+bool basis_kernel_supported(int d, int n);
 
 // Static schedule of a mesh (hd_sched.cpp): [nunits * GPU][CT][d] records (see SchedDim).
 // forced = -1: upwind by the sign of a_i; 0 / 1: every dim takes its left / right neighbour (central flux)

@@ -112,4 +112,47 @@ void build_tables(int n, Tables1D &t) {
   }
 }
 
+// Basis change between the GLL nodal basis (the paper's default shape functions) and the values at
+// the n Gauss points. GLL points: -1, 1 and the roots of P'_{n-1}, by Newton on
+// q(x) = P'_{n-1}(x) with q' from the Legendre equation (1 - x^2) P'' = 2 x P' - m (m + 1) P.
+// S[0] = T, T[q][j] = l^GLL_j(xi^Gauss_q); S[1] = T^-1 = l^Gauss_q(x^GLL_j) (both bases span P_k, so the inverse
+// is the interpolation the other way round, no linear solve); S[2] = T^T; S[3] = T^-T. Row-major [out][in].
+void build_basis_tables(int n, double S[4][kMaxN * kMaxN]) {
+  const R pi = 3.141592653589793238462643383279502884L;
+  R xr[kMaxN], wr[kMaxN], xg[kMaxN], xl[kMaxN];
+  legendre_roots(n, xr, wr);
+  for (int i = 0; i < n; ++i) xg[n - 1 - i] = (1 + xr[i]) / 2;
+  const int m = n - 1;
+  xl[0] = 0;
+  xl[n - 1] = 1;
+  for (int i = 1; i < n - 1; ++i) {
+    R t = -cosl(pi * i / m);  // Chebyshev-Lobatto guess, ascending
+    for (int it = 0; it < 200; ++it) {
+      R pm1 = 1, p = t;
+      for (int k = 2; k <= m; ++k) {
+        R pk = ((2 * k - 1) * t * p - (k - 1) * pm1) / k;
+        pm1 = p;
+        p = pk;
+      }
+      const R dp = m * (pm1 - t * p) / (1 - t * t);                    // P'_m
+      const R ddp = (2 * t * dp - (R)m * (m + 1) * p) / (1 - t * t);   // P''_m
+      const R step = dp / ddp;
+      t -= step;
+      if (fabsl(step) < 1e-30L) break;
+    }
+    xl[i] = (1 + t) / 2;
+  }
+  for (int k = 0; k < 4; ++k)
+    for (int e = 0; e < kMaxN * kMaxN; ++e) S[k][e] = 0;
+  for (int q = 0; q < n; ++q)
+    for (int j = 0; j < n; ++j) {
+      const R t = lag(xl, n, j, xg[q]);   // T[q][j]
+      const R ti = lag(xg, n, q, xl[j]);  // T^-1[j][q]
+      S[0][q * n + j] = (double)t;
+      S[2][j * n + q] = (double)t;
+      S[1][j * n + q] = (double)ti;
+      S[3][q * n + j] = (double)ti;
+    }
+}
+
 }  // namespace hd

@@ -138,3 +138,23 @@ def test_lsrk_coefficients_order_conditions(lib):
            b @ (c * (a @ c)) - 1 / 8, b @ (a @ c**2) - 1 / 12, b @ (a @ (a @ c)) - 1 / 24]
     assert np.max(np.abs(res)) < 1e-14
     assert A[0] == 0.0
+
+
+def test_basis_tables_match_independent_definitions(lib):
+    """GLL points against their closed forms and the four basis-change matrices against interpolation of
+    monomials (T maps GLL-point values of x^p to Gauss-point values, p <= k) -- no oracle code involved."""
+    from paper_2002_08110_b200._binding import basis_tables, tables_1d
+    s5, s37 = np.sqrt(1 / 5), np.sqrt(3 / 7)
+    closed = {2: [0, 1], 3: [0, 0.5, 1], 4: [0, (1 - s5) / 2, (1 + s5) / 2, 1], 5: [0, (1 - s37) / 2, 0.5, (1 + s37) / 2, 1]}
+    for n in range(2, 7):
+        gll, T = basis_tables(n)
+        if n in closed:
+            assert np.max(np.abs(gll - np.array(closed[n]))) < 1e-15
+        assert np.all(np.diff(gll) > 0) and abs(gll[0]) < 1e-15 and abs(gll[-1] - 1) < 1e-15
+        xg = tables_1d(n)["xi"]
+        for p in range(n):
+            assert np.max(np.abs(T[0] @ gll ** p - xg ** p)) < 1e-14
+            assert np.max(np.abs(T[1] @ xg ** p - gll ** p)) < 1e-14
+        assert np.array_equal(T[2], T[0].T) and np.array_equal(T[3], T[1].T)
+        assert np.max(np.abs(T[0] @ T[1] - np.eye(n))) < 1e-13
+

@@ -14,7 +14,7 @@ from paper_2002_08110_b200 import Mesh, configs  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="5d")
-ap.add_argument("--op", default="rk", choices=["rk", "adv", "mass", "fcl"])
+ap.add_argument("--op", default="rk", choices=["rk", "adv", "mass", "fcl", "basis"])
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cells", default=None, help="override cells, comma separated")
 a = ap.parse_args()
@@ -33,6 +33,8 @@ for _ in range(a.reps):
         sol = m.rk_step(bufs, sol, 0.0, dt, 1)
     elif a.op == "adv":
         m.apply_advection(bufs[0], bufs[1])
+    elif a.op == "basis":
+        m.basis_change(bufs[0], bufs[1], "gll_to_gauss")
     elif a.op == "fcl":
         m.apply_advection_fcl(bufs[0], bufs[1])
     else:
