@@ -9,7 +9,9 @@
 // a thread owns an N x N tile over dims (i, i+1), contracts both in registers and writes it back in place, so
 // a value crosses shared memory ceil(d/2) times instead of d. Cells are contiguous blocks of N^d values, so
 // the tile index runs over the whole batch (the cell index is part of its high digits). The staging buffer
-// carries one pad double per 32 (tiles of the first pass are 16 contiguous doubles per thread).
+// carries one pad double per 32 (tiles of the first pass are 16 contiguous doubles per thread). Persistent
+// CTAs (as many as stay resident) with two staging buffers: the next batch arrives by cp.async while the
+// current one is contracted and streamed out (one buffer where two do not fit).
 #include <cuda_runtime.h>
 
 #include "hd_internal.h"
@@ -20,88 +22,130 @@ namespace {
 
 __device__ __forceinline__ int padded(int x) { return x + (x >> 5); }
 
+// dims (i, i+1) of every tile of the batch, ST = N^i: x <- (S x S) x in place
+template <int N, int ST>
+__device__ __forceinline__ void tile_pass(double *sm, int cnt, const double *S) {
+  const int nt = cnt / (N * N);
+  for (int l = threadIdx.x; l < nt; l += blockDim.x) {
+    const int lo = l % ST, hi = l / ST;
+    const int base = hi * (ST * N * N) + lo;
+    double x[N][N];
+#pragma unroll
+    for (int q1 = 0; q1 < N; ++q1)
+#pragma unroll
+      for (int q0 = 0; q0 < N; ++q0) x[q1][q0] = sm[padded(base + (q0 + N * q1) * ST)];
+#pragma unroll
+    for (int q1 = 0; q1 < N; ++q1) {  // dim i, row by row in place
+      double t[N];
+#pragma unroll
+      for (int m0 = 0; m0 < N; ++m0) {
+        double a = 0.0;
+#pragma unroll
+        for (int q0 = 0; q0 < N; ++q0) a = fma(S[m0 * N + q0], x[q1][q0], a);
+        t[m0] = a;
+      }
+#pragma unroll
+      for (int m0 = 0; m0 < N; ++m0) x[q1][m0] = t[m0];
+    }
+#pragma unroll
+    for (int m0 = 0; m0 < N; ++m0)  // dim i+1, column by column straight to shared memory
+#pragma unroll
+      for (int m1 = 0; m1 < N; ++m1) {
+        double a = 0.0;
+#pragma unroll
+        for (int q1 = 0; q1 < N; ++q1) a = fma(S[m1 * N + q1], x[q1][m0], a);
+        sm[padded(base + (m0 + N * m1) * ST)] = a;
+      }
+  }
+}
+
+// the last dim of an odd d alone, ST = N^(d-1)
+template <int N, int ST>
+__device__ __forceinline__ void line_pass(double *sm, int cnt, const double *S) {
+  const int nl = cnt / N;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const int lo = l % ST, hi = l / ST;
+    const int base = hi * (ST * N) + lo;
+    double x[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) x[q] = sm[padded(base + q * ST)];
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) a = fma(S[m * N + q], x[q], a);
+      sm[padded(base + m * ST)] = a;
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory"); }
+
 template <int N>
-__global__ void __launch_bounds__(256) basis_kernel(const __grid_constant__ BasisParams p) {
-  extern __shared__ double sm[];
+__global__ void __launch_bounds__(256, N <= 3 ? 4 : N == 4 ? 3 : N == 5 ? 2 : 1)
+    basis_kernel(const __grid_constant__ BasisParams p) {
+  extern __shared__ double smem[];
+  constexpr int N2 = N * N, N4 = N2 * N2;
   int ND = 1;
   for (int i = 0; i < p.d; ++i) ND *= N;
   const long long nb = (p.ncells + p.cb - 1) / p.cb;
-  for (long long b = blockIdx.x; b < nb; b += gridDim.x) {
-    const long long c0 = b * p.cb;
-    const long long left = p.ncells - c0;
-    const int cnt = (int)(left < p.cb ? left : p.cb) * ND;
-    const double *src = p.u + c0 * ND;
-    double *dst = p.v + c0 * ND;
-    __syncthreads();  // the previous batch's copy-out has read the buffer
-    if constexpr (N % 2 == 0) {  // ND even: 16-B aligned batches
-      for (int e = 2 * threadIdx.x; e < cnt; e += 2 * blockDim.x) {
-        const double2 x = __ldcs(reinterpret_cast<const double2 *>(src + e));
-        sm[padded(e)] = x.x;
-        sm[padded(e + 1)] = x.y;
-      }
+  const int full = p.cb * ND;
+  const int bufsz = full + (full >> 5) + 1;  // padded doubles per buffer
+  auto count_of = [&](long long b) {
+    const long long left = p.ncells - b * p.cb;
+    return (int)(left < p.cb ? left : p.cb) * ND;
+  };
+  // stage batch b: every value by its own 8-byte cp.async (the padded layout keeps 8-byte alignment only), all
+  // of a thread's copies in flight at once and none held in registers
+  auto issue = [&](long long b, double *buf) {
+    const double *src = p.u + b * (long long)full;
+    const int cnt = count_of(b);
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) cp_async8(buf + padded(e), src + e);
+  };
+  long long b = blockIdx.x;
+  int cur = 0;
+  if (b < nb) issue(b, smem);
+  cp_async_commit();
+  for (; b < nb; b += gridDim.x) {
+    const long long nxt = b + gridDim.x;
+    double *sm = smem + cur * bufsz;
+    if (p.nbuf == 2) {  // the next batch streams in while this one is contracted and written out
+      if (nxt < nb) issue(nxt, smem + (cur ^ 1) * bufsz);
+      cp_async_commit();
+      cp_async_wait<1>();
     } else {
-      for (int e = threadIdx.x; e < cnt; e += blockDim.x) sm[padded(e)] = __ldcs(src + e);
+      cp_async_wait<0>();
     }
     __syncthreads();
-    int st = 1;  // N^i
-    int i = 0;
-    for (; i + 1 < p.d; i += 2) {  // dims (i, i+1) together
-      const int nt = cnt / (N * N);
-      for (int l = threadIdx.x; l < nt; l += blockDim.x) {
-        const int lo = l % st, hi = l / st;
-        const int base = hi * st * N * N + lo;
-        double x[N][N], y[N][N];
-#pragma unroll
-        for (int q1 = 0; q1 < N; ++q1)
-#pragma unroll
-          for (int q0 = 0; q0 < N; ++q0) x[q1][q0] = sm[padded(base + (q0 + N * q1) * st)];
-#pragma unroll
-        for (int q1 = 0; q1 < N; ++q1)
-#pragma unroll
-          for (int m0 = 0; m0 < N; ++m0) {
-            double s = 0.0;
-#pragma unroll
-            for (int q0 = 0; q0 < N; ++q0) s = fma(p.S[m0 * N + q0], x[q1][q0], s);
-            y[q1][m0] = s;
-          }
-#pragma unroll
-        for (int m1 = 0; m1 < N; ++m1)
-#pragma unroll
-          for (int m0 = 0; m0 < N; ++m0) {
-            double s = 0.0;
-#pragma unroll
-            for (int q1 = 0; q1 < N; ++q1) s = fma(p.S[m1 * N + q1], y[q1][m0], s);
-            sm[padded(base + (m0 + N * m1) * st)] = s;
-          }
-      }
-      st *= N * N;
-      __syncthreads();
-    }
-    if (i < p.d) {  // odd d: the last dim alone
-      const int nl = cnt / N;
-      for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-        const int lo = l % st, hi = l / st;
-        const int base = hi * st * N + lo;
-        double x[N];
-#pragma unroll
-        for (int q = 0; q < N; ++q) x[q] = sm[padded(base + q * st)];
-#pragma unroll
-        for (int m = 0; m < N; ++m) {
-          double s = 0.0;
-#pragma unroll
-          for (int q = 0; q < N; ++q) s = fma(p.S[m * N + q], x[q], s);
-          sm[padded(base + m * st)] = s;
-        }
-      }
-      __syncthreads();
-    }
-    if constexpr (N % 2 == 0) {
+    const int cnt = count_of(b);
+    if (p.d >= 2) { tile_pass<N, 1>(sm, cnt, p.S); __syncthreads(); }
+    if (p.d >= 4) { tile_pass<N, N2>(sm, cnt, p.S); __syncthreads(); }
+    if (p.d >= 6) { tile_pass<N, N4>(sm, cnt, p.S); __syncthreads(); }
+    if (p.d == 1) { line_pass<N, 1>(sm, cnt, p.S); __syncthreads(); }
+    if (p.d == 3) { line_pass<N, N2>(sm, cnt, p.S); __syncthreads(); }
+    if (p.d == 5) { line_pass<N, N4>(sm, cnt, p.S); __syncthreads(); }
+    double *dst = p.v + b * (long long)full;
+    if constexpr (N % 2 == 0) {  // ND even: 16-B aligned batches
       for (int e = 2 * threadIdx.x; e < cnt; e += 2 * blockDim.x)
         __stcs(reinterpret_cast<double2 *>(dst + e), make_double2(sm[padded(e)], sm[padded(e + 1)]));
     } else {
       for (int e = threadIdx.x; e < cnt; e += blockDim.x) __stcs(dst + e, sm[padded(e)]);
     }
+    __syncthreads();  // the buffer has been read out before it is refilled
+    if (p.nbuf == 2) {
+      cur ^= 1;
+    } else {
+      if (nxt < nb) issue(nxt, smem);
+      cp_async_commit();
+    }
   }
+  cp_async_wait<0>();
 }
 
 constexpr int kBatchDoubles = 4096;
@@ -122,12 +166,15 @@ cudaError_t launch_n(BasisParams &p, cudaStream_t s, int sms) {
   if (cb < 1) cb = 1;
   if (cb > p.ncells) cb = p.ncells;
   p.cb = (int)cb;
-  const size_t smem = smem_of(cb * ND);
+  const size_t one = smem_of(cb * ND);
+  p.nbuf = 2 * one <= kMaxSmem ? 2 : 1;
+  const size_t smem = p.nbuf * one;
   cudaError_t e = cudaFuncSetAttribute(basis_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
   if (e != cudaSuccess) return e;
   const long long nb = (p.ncells + cb - 1) / cb;
-  int per_sm = (int)(kMaxSmem / (smem + 1024));
-  if (per_sm > 8) per_sm = 8;
+  int per_sm = (int)((227 * 1024) / (smem + 1024));
+  const int by_regs = N <= 3 ? 4 : N == 4 ? 3 : N == 5 ? 2 : 1;  // the kernel's launch bounds
+  if (per_sm > by_regs) per_sm = by_regs;
   if (per_sm < 1) per_sm = 1;
   const long long cap = (long long)sms * per_sm;
   basis_kernel<N><<<(unsigned)(nb < cap ? nb : cap), 256, smem, s>>>(p);

@@ -39,7 +39,7 @@ struct BasisParams {
   const double *u;
   double *v;
   long long ncells;
-  int d, cb;                 // dims, cells per CTA batch
+  int d, cb, nbuf;           // dims, cells per CTA batch, staging buffers (2: next batch prefetched)
   double S[kMaxN * kMaxN];   // [out * n + in]
 };
 

@@ -8,7 +8,7 @@ import pytest
 from oracle import gll as ogll
 from paper_2002_08110_b200 import configs, inputs
 
-from test_gpu_parity import DEGENERATE, SMALL, TOL_APPLY, TOL_RK, assert_close, dev, host, mesh, spec_of
+from test_gpu_parity import DEGENERATE, SMALL, TOL_APPLY, TOL_RK10, assert_close, dev, host, mesh, spec_of
 
 pytestmark = pytest.mark.gpu
 
@@ -67,7 +67,7 @@ def test_gll_config_full_parity(name):
     dt = configs.time_step(spec)
     bufs = [ud.clone(), torch.empty_like(ud), torch.empty_like(ud)]
     sol = m.rk_step_gll(bufs, 0, 0.0, dt, 10)
-    assert_close(host(bufs[sol]), ogll.rk_steps_gll(spec, u, 0.0, dt, 10), TOL_RK, name + " RK10 GLL")
+    assert_close(host(bufs[sol]), ogll.rk_steps_gll(spec, u, 0.0, dt, 10), TOL_RK10, name + " RK10 GLL")
 
 
 def test_basis_change_6d_full_size_sampled():
