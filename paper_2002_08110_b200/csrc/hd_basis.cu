@@ -131,12 +131,9 @@ __global__ void __launch_bounds__(256, N <= 3 ? 4 : N == 4 ? 3 : N == 5 ? 2 : 1)
     if (p.d == 3) { line_pass<N, N2>(sm, cnt, p.S); __syncthreads(); }
     if (p.d == 5) { line_pass<N, N4>(sm, cnt, p.S); __syncthreads(); }
     double *dst = p.v + b * (long long)full;
-    if constexpr (N % 2 == 0) {  // ND even: 16-B aligned batches
-      for (int e = 2 * threadIdx.x; e < cnt; e += 2 * blockDim.x)
-        __stcs(reinterpret_cast<double2 *>(dst + e), make_double2(sm[padded(e)], sm[padded(e + 1)]));
-    } else {
-      for (int e = threadIdx.x; e < cnt; e += blockDim.x) __stcs(dst + e, sm[padded(e)]);
-    }
+    // 8-byte stores: consecutive threads read consecutive (conflict-free) padded slots and write one
+    // contiguous 256-B segment per warp
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) __stcs(dst + e, sm[padded(e)]);
     __syncthreads();  // the buffer has been read out before it is refilled
     if (p.nbuf == 2) {
       cur ^= 1;

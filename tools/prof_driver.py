@@ -17,6 +17,7 @@ ap.add_argument("--config", default="5d")
 ap.add_argument("--op", default="rk", choices=["rk", "adv", "mass", "fcl", "basis"])
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cells", default=None, help="override cells, comma separated")
+ap.add_argument("--time", action="store_true", help="print ms per application (CUDA events, after the reps as warm-up)")
 a = ap.parse_args()
 cfg = configs.CONFIGS[a.config]
 spec = dict(cfg["spec"])
@@ -40,4 +41,17 @@ for _ in range(a.reps):
     else:
         m.apply_inv_mass(bufs[0])
 torch.cuda.synchronize()
+if a.time:
+    fn = {"adv": lambda: m.apply_advection(bufs[0], bufs[1]), "mass": lambda: m.apply_inv_mass(bufs[0]),
+          "basis": lambda: m.basis_change(bufs[0], bufs[1], "gll_to_gauss"),
+          "fcl": lambda: m.apply_advection_fcl(bufs[0], bufs[1])}.get(a.op)
+    if fn is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        print(f"{a.config} {a.op}: {ms:.3f} ms, {N / ms / 1e6:.1f} GDoF/s, {16 * N / ms / 1e6:.0f} GB/s at 16 B/DoF")
 print("ok", N, float(bufs[sol][:1000].sum()))
