@@ -109,3 +109,28 @@ def test_basis_change_rejects_bad_calls():
         m.basis_change(a, a, 7)          # unknown kind
     with pytest.raises(HDError):
         m.apply_advection_gll(a, u[m.owned_dofs:], a)   # work aliases u
+
+
+@pytest.mark.parametrize("P,xparts,vparts", [(2, None, None), (4, [2, 1], [1, 2])])
+def test_basis_change_on_partitioned_meshes(P, xparts, vparts):
+    """The basis change is cell-local: on the ranks of an x-slab and of a checkerboard x-v partition it equals the
+    single-rank result bitwise, and the oracle to 1e-13 (hd.h: "any partition")."""
+    import torch
+    from paper_2002_08110_b200 import Mesh, configs
+    from test_gpu_multirank import _join, _split, _vlasov
+    spec = _vlasov(2, 2, 3, [4, 6, 2, 4], extra=0.1)
+    u = np.random.default_rng(21).uniform(-1, 1, configs.dof_count(spec))
+    one = Mesh(spec)
+    ud = dev(u)
+    ref = torch.empty_like(ud)
+    one.basis_change(ud, ref, "gll_to_gauss")
+    meshes = [Mesh(spec, rank=r, nranks=P, xparts=xparts, vparts=vparts) for r in range(P)]
+    parts = _split(spec, u, meshes)
+    outs = []
+    for m, part in zip(meshes, parts):
+        x = dev(part)
+        m.basis_change(x, x, "gll_to_gauss")
+        outs.append(host(x))
+    got = _join(spec, outs, meshes)
+    assert np.array_equal(got, host(ref))
+    assert_close(got, ogll.basis_change(spec, u, "gll_to_gauss"), TOL_BASIS, "partitioned T")
