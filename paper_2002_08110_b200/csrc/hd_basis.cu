@@ -37,11 +37,16 @@ __device__ __forceinline__ void tile_pass(double *sm, int cnt, const double *S) 
     const int lo = l % ST, hi = l / ST;
     const int base = hi * (ST * N * N) + lo;
     constexpr bool kVec = ST == 1 && N % 2 == 0;  // the tile is N^2 contiguous doubles starting at an even index
+    // tile elements a multiple of 16 apart from a base (or, first pass, inside one aligned 16-block): the padded
+    // index is padded(base) plus a compile-time offset, so the accesses use immediate offsets
+    constexpr bool kConst = N % 2 == 0 && (ST % 16 == 0 || (ST == 1 && N * N == 16));
+    const int pb = padded<N>(base);
+    auto at = [&](int off) { return kConst ? pb + off + 2 * (off >> 4) : padded<N>(base + off); };
     double x[N][N];
     if constexpr (kVec) {
 #pragma unroll
       for (int q = 0; q < N * N; q += 2) {
-        const double2 v = *reinterpret_cast<const double2 *>(&sm[padded<N>(base + q)]);
+        const double2 v = *reinterpret_cast<const double2 *>(&sm[at(q)]);
         x[q / N][q % N] = v.x;
         x[(q + 1) / N][(q + 1) % N] = v.y;
       }
@@ -49,7 +54,7 @@ __device__ __forceinline__ void tile_pass(double *sm, int cnt, const double *S) 
 #pragma unroll
       for (int q1 = 0; q1 < N; ++q1)
 #pragma unroll
-        for (int q0 = 0; q0 < N; ++q0) x[q1][q0] = sm[padded<N>(base + (q0 + N * q1) * ST)];
+        for (int q0 = 0; q0 < N; ++q0) x[q1][q0] = sm[at((q0 + N * q1) * ST)];
     }
 #pragma unroll
     for (int q1 = 0; q1 < N; ++q1) {  // dim i, row by row in place
@@ -75,7 +80,7 @@ __device__ __forceinline__ void tile_pass(double *sm, int cnt, const double *S) 
             a = fma(S[m1 * N + q1], x[q1][m0], a);
             c = fma(S[m1 * N + q1], x[q1][m0 + 1], c);
           }
-          *reinterpret_cast<double2 *>(&sm[padded<N>(base + m0 + N * m1)]) = make_double2(a, c);
+          *reinterpret_cast<double2 *>(&sm[at(m0 + N * m1)]) = make_double2(a, c);
         }
     } else {
 #pragma unroll
@@ -85,7 +90,7 @@ __device__ __forceinline__ void tile_pass(double *sm, int cnt, const double *S) 
           double a = 0.0;
 #pragma unroll
           for (int q1 = 0; q1 < N; ++q1) a = fma(S[m1 * N + q1], x[q1][m0], a);
-          sm[padded<N>(base + (m0 + N * m1) * ST)] = a;
+          sm[at((m0 + N * m1) * ST)] = a;
         }
     }
   }
